@@ -1,0 +1,367 @@
+"""Pins for the CPU oracle (oracle/oracle.c) against things other than itself:
+worked examples printed in SPEC.md (tests/golden), exact integer arithmetic, LAPACK
+(numpy/scipy) as an independent third party, closed forms, invariants, metamorphic
+identities and the paper's stated accuracy claims. No test here retypes the oracle's
+formulas. CPU only.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+U_RND = 2.0 ** -53
+
+
+def M(x):
+    return np.asfortranarray(np.array(x, dtype=np.float64))
+
+
+# ---------------------------------------------------------------- SPEC worked examples
+def test_spec_gram(orc):
+    for ex in GOLD["gram"]:
+        assert np.array_equal(orc.gram(M(ex["a"])), M(ex["expect"])), ex["cite"]
+
+
+def test_spec_projection_and_update(orc):
+    for ex in GOLD["matmul_t"]:
+        assert np.array_equal(orc.atb(M(ex["a"]), M(ex["b"])), M(ex["expect"])), ex["cite"]
+    for ex in GOLD["sub_prod"]:
+        assert np.array_equal(orc.sub_prod(M(ex["c"]), M(ex["q"]), M(ex["y"])), M(ex["expect"])), ex["cite"]
+
+
+def test_spec_cholesky(orc):
+    for ex in GOLD["chol"]:
+        U, brk = orc.chol(M(ex["w"]))
+        if "breakdown_pivot" in ex:
+            assert U is None and brk == (ex["breakdown_pivot"], ex["pivot_value"]), ex["cite"]
+        else:
+            assert brk is None and np.array_equal(U, M(ex["expect"])), ex["cite"]
+
+
+def test_spec_rsolve_trimul(orc):
+    for ex in GOLD["rsolve"]:
+        assert np.array_equal(orc.rsolve(M(ex["a"]), M(ex["u"])), M(ex["expect"])), ex["cite"]
+    for ex in GOLD["tri_mul"]:
+        assert np.array_equal(orc.tri_mul(M(ex["r2"]), M(ex["r1"])), M(ex["expect"])), ex["cite"]
+
+
+def test_spec_cqr_and_householder(orc):
+    for ex in GOLD["cqr"]:
+        Q, R, info = orc.factor(M(ex["a"]), 1, "cqr")
+        assert info["status"] == 0
+        assert np.array_equal(R, M(ex["r"]))
+        np.testing.assert_allclose(Q, M(ex["q"]), rtol=0, atol=2 * U_RND)
+    for ex in GOLD["householder"]:
+        Q, R = orc.householder(M(ex["a"]))
+        np.testing.assert_allclose(R, M(ex["r"]), rtol=0, atol=8 * U_RND)
+        np.testing.assert_allclose(Q, M(ex["q"]), rtol=0, atol=4 * U_RND)
+
+
+def test_spec_metrics(orc):
+    for ex in GOLD["orthogonality_unnormalised"]:
+        assert orc.orthogonality(M(ex["q"])) == pytest.approx(ex["expect"], abs=1e-15), ex["cite"]
+    for ex in GOLD["residual"]:
+        r = orc.residual(M(ex["a"]), M(ex["q"]), M(ex["r"]))
+        if "expect" in ex:
+            assert r == ex["expect"], ex["cite"]
+        else:
+            assert r <= ex["expect_max"], ex["cite"]
+
+
+# ---------------------------------------------------------------- exact integer pins
+@pytest.mark.parametrize("m,p,q", [(1000, 16, 16), (4099, 7, 33), (777, 64, 5)])
+def test_atb_exact_integers(orc, m, p, q):
+    """Entries in [-3,3]: every partial sum is an integer < 2^53, so any summation
+    order is exact; compare bitwise with int64 arithmetic."""
+    X = synth.integer_matrix(m, p, seed=1)
+    Y = synth.integer_matrix(m, q, seed=2)
+    ref = (X.astype(np.int64).T @ Y.astype(np.int64)).astype(np.float64)
+    assert np.array_equal(orc.atb(X, Y), ref)
+    G = (X.astype(np.int64).T @ X.astype(np.int64)).astype(np.float64)
+    W = orc.gram(X)
+    assert np.array_equal(W, G) and np.array_equal(W, W.T)
+
+
+def test_sub_prod_exact_integers(orc):
+    X = synth.integer_matrix(513, 40, seed=3)
+    Q = synth.integer_matrix(513, 24, seed=4)
+    Y = synth.integer_matrix(24, 40, seed=5)
+    ref = (X.astype(np.int64) - Q.astype(np.int64) @ Y.astype(np.int64)).astype(np.float64)
+    assert np.array_equal(orc.sub_prod(X, Q, Y), ref)
+
+
+def _unit_upper_int(b, seed):
+    rng = np.random.default_rng(seed)
+    U = np.triu(rng.integers(-2, 3, size=(b, b)).astype(np.float64), 1) + np.eye(b)
+    return np.asfortranarray(U)
+
+
+def test_rsolve_exact(orc):
+    """X = Z U with integer Z and unit upper-triangular integer U: rsolve(X,U) must give Z
+    exactly (every intermediate is a small integer)."""
+    b = 12
+    U = _unit_upper_int(b, 0)
+    Z = synth.integer_matrix(300, b, seed=6)
+    X = (Z.astype(np.int64) @ U.astype(np.int64)).astype(np.float64)
+    assert np.array_equal(orc.rsolve(X, U), Z)
+
+
+def test_tri_inv_exact(orc):
+    """A unit upper-triangular integer matrix has an integer inverse: U Z = I exactly."""
+    for b in (8, 16):
+        U = _unit_upper_int(b, b)
+        Z = orc.tri_inv(U)
+        assert np.array_equal(Z, np.round(Z))
+        assert np.array_equal(U.astype(np.int64) @ Z.astype(np.int64), np.eye(b, dtype=np.int64))
+        assert np.array_equal(np.tril(Z, -1), np.zeros((b, b)))
+
+
+# ---------------------------------------------------------------- LAPACK pins
+@pytest.mark.parametrize("b,kappa", [(16, 1e2), (64, 1e6), (128, 1e7)])
+def test_cholesky_vs_lapack(orc, b, kappa):
+    A, _, _ = synth.generate_np(4096, b, kappa, seed=3)
+    W = A.T @ A
+    W = np.triu(W) + np.triu(W, 1).T  # exactly symmetric
+    U, brk = orc.chol(W)
+    assert brk is None
+    Ul = sla.cholesky(W, lower=False)  # LAPACK dpotrf
+    assert np.array_equal(np.tril(U, -1), np.zeros_like(U))
+    assert np.all(np.diag(U) > 0)
+    assert np.linalg.norm(U.T @ U - W) <= 10 * U_RND * np.linalg.norm(W) * b
+    # forward error relative to LAPACK: first-order bound b * u * cond(U) with cond(U) = kappa
+    assert np.linalg.norm(U - Ul) <= b * U_RND * kappa * np.linalg.norm(Ul)
+
+
+def test_tri_inv_vs_lapack(orc):
+    A, _, _ = synth.generate_np(2048, 64, 1e4, seed=4)
+    U = np.linalg.qr(A, mode="r")
+    U = np.asfortranarray(U * np.sign(np.diag(U))[:, None])
+    Z = orc.tri_inv(U)
+    Zl = sla.lapack.dtrtri(U, lower=0)[0]
+    cond = np.linalg.cond(U)
+    assert np.linalg.norm(Z - Zl) <= 64 * U_RND * cond * np.linalg.norm(Zl)
+
+
+def test_householder_vs_numpy(orc):
+    rng = np.random.default_rng(7)
+    for _ in range(10):
+        m, n = int(rng.integers(20, 200)), int(rng.integers(2, 20))
+        A = np.asfortranarray(rng.standard_normal((m, n)))
+        Q, R = orc.householder(A)
+        Qn, Rn = np.linalg.qr(A)
+        s = np.sign(np.diag(Rn))
+        Qn, Rn = Qn * s, Rn * s[:, None]
+        np.testing.assert_allclose(R, Rn, atol=1e-12 * np.linalg.norm(A))
+        np.testing.assert_allclose(Q, Qn, atol=1e-12)
+        assert orc.orthogonality(Q) / math.sqrt(n) <= 50 * U_RND
+        assert orc.residual(A, Q, R) <= 50 * U_RND
+
+
+# ---------------------------------------------------------------- whole algorithms
+ALL = ["cqr", "cqr2", "cqrgs", "cqr2gs", "mcqr2gs"]
+
+
+def test_algorithms_match_householder_small(orc):
+    """S:362 / S:596: on 50 small well-conditioned inputs every algorithm's R equals the
+    (unique, sign-normalised) Householder R within 1e-10 ||A||_F entrywise."""
+    rng = np.random.default_rng(11)
+    for t in range(50):
+        m, n = int(rng.integers(40, 200)), int(rng.integers(2, 20))
+        kappa = 10.0 ** rng.uniform(0, 3)
+        A, _, _ = synth.generate_np(m, n, kappa, seed=100 + t, chunk=m)
+        _, Rh = orc.householder(A)
+        b = int(rng.integers(1, n + 1))
+        for algo in ALL:
+            Q, R, info = orc.factor(A, b, algo)
+            assert info["status"] == 0, (algo, info)
+            assert np.max(np.abs(R - Rh)) <= 1e-10 * np.linalg.norm(A), algo
+            assert orc.residual(A, Q, R) <= 1e-13, algo
+
+
+def test_degeneracies_bitwise(orc):
+    """P:357 / S:334: with one panel CQR2GS and mCQR2GS are CQR2, CQRGS is CQR."""
+    A, _, _ = synth.generate_np(2048, 48, 1e6, seed=5)
+    Q2, R2, _ = orc.factor(A, 48, "cqr2")
+    for algo in ("cqr2gs", "mcqr2gs"):
+        Q, R, _ = orc.factor(A, 48, algo)
+        assert np.array_equal(Q, Q2) and np.array_equal(R, R2), algo
+    Q1, R1, _ = orc.factor(A, 48, "cqr")
+    Q, R, _ = orc.factor(A, 48, "cqrgs")
+    assert np.array_equal(Q, Q1) and np.array_equal(R, R1)
+
+
+def test_orthonormal_input(orc):
+    """kappa = 1: R = I and Q = A within 10u."""
+    A, _, _ = synth.generate_np(4096, 64, 1.0, seed=6)
+    for algo, b in [("cqr2", 64), ("cqr2gs", 16), ("mcqr2gs", 16), ("mcqr2gs", 32)]:
+        Q, R, info = orc.factor(A, b, algo)
+        assert info["status"] == 0
+        assert np.max(np.abs(R - np.eye(64))) <= 10 * U_RND * 8
+        assert np.max(np.abs(Q - A)) <= 10 * U_RND * 8
+
+
+def test_column_power_of_two_scaling_bitwise(orc):
+    """Metamorphic pin: scaling columns by D = diag(2^e) commutes exactly with every
+    rounded step, so Q(AD) = Q(A) and R(AD) = R(A) D bitwise (an index or transposition
+    error in Gram, update, re-orthogonalisation or R assembly breaks this)."""
+    A, _, _ = synth.generate_np(4096, 64, 1e12, seed=8)
+    e = np.random.default_rng(0).integers(-6, 7, size=64)
+    D = np.ldexp(1.0, e)
+    AD = np.asfortranarray(A * D)
+    for algo, b in [("cqr2gs", 16), ("mcqr2gs", 16), ("mcqr2gs", 32)]:
+        Q, R, i1 = orc.factor(A, b, algo)
+        QD, RD, i2 = orc.factor(AD, b, algo)
+        assert i1["status"] == 0 and i2["status"] == 0
+        assert np.array_equal(Q, QD), algo
+        assert np.array_equal(R * D, RD), algo
+
+
+def test_r_equals_r_of_sigma_vt(orc):
+    """A = U (Sigma V^T) with orthonormal U, so R(A) = R(Sigma V^T), an n x n matrix
+    factored here by LAPACK (numpy.linalg.qr) -- an m-free, implementation-free pin."""
+    n = 64
+    for kappa in (1e2, 1e5, 1e8):
+        A, sigma, V = synth.generate_np(8192, n, kappa, seed=9, chunk=4096)
+        B = sigma[:, None] * V.T
+        Rb = np.linalg.qr(B, mode="r")
+        Rb = Rb * np.sign(np.diag(Rb))[:, None]
+        for algo, b in [("cqr2", n), ("cqr2gs", 16), ("mcqr2gs", 16)]:
+            _, R, info = orc.factor(A, b, algo)
+            assert info["status"] == 0
+            rel = np.linalg.norm(R - Rb) / np.linalg.norm(Rb)
+            assert rel <= 1e-12, (kappa, algo, rel)
+
+
+def test_determinant_identity(orc):
+    """|det R| = prod sigma_i, i.e. sum log R_ii = -(n/2) log kappa (closed form)."""
+    n = 64
+    for kappa, tol in ((1e4, 1e-9), (1e8, 1e-6), (1e15, 1.0)):
+        A, _, _ = synth.generate_np(4096, n, kappa, seed=10)
+        _, R, info = orc.factor(A, 16, "mcqr2gs")
+        assert info["status"] == 0
+        assert abs(np.sum(np.log(np.diag(R))) + 0.5 * n * math.log(kappa)) <= tol
+
+
+def test_invariants_and_counts(orc):
+    """R strictly upper with exact zeros and positive diagonal; Allreduce count
+    4k-2 for CQR2GS and mCQR2GS, 2 for CQR2, 2k-1 for CQRGS (Appendix A.2 of SURVEY,
+    S:331)."""
+    n, b = 64, 16
+    k = n // b
+    A, _, _ = synth.generate_np(4096, n, 1e8, seed=12)
+    for algo, expect in [("cqr2", 2), ("cqr", 1), ("cqrgs", 2 * k - 1), ("cqr2gs", 4 * k - 2),
+                         ("mcqr2gs", 4 * k - 2)]:
+        orc.reset_reduction_count()
+        Q, R, info = orc.factor(A, b, algo)
+        assert orc.reduction_count() == expect, algo
+        assert info["status"] == 0
+        assert np.array_equal(np.tril(R, -1), np.zeros_like(R))
+        assert np.all(np.diag(R) > 0)
+
+
+def test_ragged_panels(orc):
+    """the last panel may be narrower; results stay accurate."""
+    A, _, _ = synth.generate_np(4096, 50, 1e10, seed=13)
+    for algo in ("cqr2gs", "mcqr2gs"):
+        Q, R, info = orc.factor(A, 16, algo)
+        assert info["status"] == 0
+        assert orc.orthogonality(Q) <= 1e-13 and orc.residual(A, Q, R) <= 1e-14
+
+
+def test_thread_count_independence(orc):
+    A, _, _ = synth.generate_np(65536, 64, 1e12, seed=14)
+    old = orc.get_threads()
+    try:
+        orc.set_threads(1)
+        Q1, R1, _ = orc.factor(A, 16, "mcqr2gs")
+        orc.set_threads(max(2, old))
+        Q2, R2, _ = orc.factor(A, 16, "mcqr2gs")
+    finally:
+        orc.set_threads(old)
+    assert np.array_equal(Q1, Q2) and np.array_equal(R1, R2)
+
+
+def test_breakdown_reporting(orc):
+    """A zero column makes the Gram singular with an exactly zero pivot: CQR's Cholesky
+    breaks down; the oracle reports it as a value with (panel, stage, pivot)."""
+    A, _, _ = synth.generate_np(1024, 16, 1e2, seed=15)
+    A[:, 5] = 0.0
+    Q, R, info = orc.factor(A, 16, "cqr2")
+    assert Q is None and info["status"] == 5
+    assert info["panel"] == 1 and info["stage"] == 1 and info["pivot"] == 5
+    assert not (info["pivot_value"] > 0)
+    A2, _, _ = synth.generate_np(1024, 32, 1e2, seed=15)
+    A2[:, 20] = 0.0
+    _, _, info2 = orc.factor(A2, 16, "mcqr2gs")
+    assert info2["status"] == 5 and info2["panel"] == 2 and info2["stage"] == 1 and info2["pivot"] == 4
+
+
+# ---------------------------------------------------------------- paper's accuracy claims
+def _run(orc, A, b, algo):
+    Q, R, info = orc.factor(A, b, algo)
+    if info["status"] != 0:
+        return None
+    return orc.orthogonality(Q) / math.sqrt(A.shape[1])
+
+
+@pytest.mark.parametrize("kappa", [1e0, 1e4, 1e8, 1e12, 1e15])
+def test_paper_claim_mcqr2gs_three_panels(orc, kappa):
+    """mCQR2GS with 3 panels reaches O(u) orthogonality and residual through
+    kappa = 1e15 (SPEC's desk-scale 3000 x 300)."""
+    A, _, _ = synth.generate_np(3000, 300, kappa, seed=0, chunk=3000)
+    Q, R, info = orc.factor(A, 100, "mcqr2gs")
+    assert info["status"] == 0
+    assert orc.orthogonality(Q) / math.sqrt(300) <= 1e-13
+    assert orc.residual(A, Q, R) <= 1e-13
+
+
+def test_paper_claim_cqr2_fails_beyond_1e8(orc):
+    """CQR2 is stable to kappa ~ 1e8 and fails (breakdown or loss of
+    orthogonality) beyond."""
+    A, _, _ = synth.generate_np(3000, 300, 1e4, seed=0, chunk=3000)
+    assert _run(orc, A, 300, "cqr2") <= 1e-13
+    A, _, _ = synth.generate_np(3000, 300, 1e12, seed=0, chunk=3000)
+    o = _run(orc, A, 300, "cqr2")
+    assert o is None or o > 1e-8
+
+
+def test_paper_claim_mcqr2gs_two_panels_break(orc):
+    """with 2 panels mCQR2GS breaks down at very high kappa, 3 panels do not
+    (S:355). Frozen desk-scale observation (R-17): at 6000 x 600 the
+    2-panel breakdown appears at kappa = 1e16, one decade above the paper's 1e15 at
+    30000 x 3000 -- inside SPEC's +-1 decade allowance."""
+    A, _, _ = synth.generate_np(6000, 600, 1e16, seed=0, chunk=6000)
+    o = _run(orc, A, 300, "mcqr2gs")
+    assert o is None or o > 1e-8
+    assert _run(orc, A, 200, "mcqr2gs") <= 1e-13
+
+
+def test_paper_claim_cqr2gs_needs_more_panels(orc):
+    """at kappa = 1e15 CQR2GS needs many panels; k=1 always breaks down
+    (S:594). Frozen desk-scale observation: k = 10 passes."""
+    A, _, _ = synth.generate_np(3000, 300, 1e15, seed=0, chunk=3000)
+    assert _run(orc, A, 300, "cqr2gs") is None
+    assert _run(orc, A, 30, "cqr2gs") <= 1e-13
+    A, _, _ = synth.generate_np(6000, 600, 1e16, seed=0, chunk=6000)
+    for b in (600, 300):
+        o = _run(orc, A, b, "cqr2gs")
+        assert o is None or o > 1e-8
+    assert _run(orc, A, 60, "cqr2gs") <= 1e-13
+
+
+def test_interlacing_panel_condition(orc):
+    """Eq. 7: cond(A) >= cond(A_1) >= sigma_{1+(n-b)} / sigma_b for the leading
+    panel A_1 of the generated matrices."""
+    n = 30
+    for kappa in (1e0, 1e4, 1e8):
+        A, sigma, _ = synth.generate_np(300, n, kappa, seed=1, chunk=300)
+        for b in (3, 15):
+            c = np.linalg.cond(A[:, :b])
+            lower = sigma[n - b] / sigma[b - 1]
+            assert c <= kappa * 1.05 + 1e-9 and c * 1.05 >= lower
