@@ -1,0 +1,180 @@
+/*
+ * tsqr.h -- C ABI of libtsqr: distributed FP64 QR of a tall-and-skinny matrix on
+ * B200 GPUs, following arXiv 2405.04237 (Mijic, Kaushik, Davidovic).
+ *
+ * Problem: A = Q R with A in R^{m x n}, m >= n, Q with orthonormal
+ * columns, R upper triangular.  A is distributed in 1-D block rows, one block per
+ * GPU (Fig. distA); Q stays distributed and overwrites A in place
+ * (P:142); R is computed redundantly and replicated on every rank.
+ *
+ * Methods (TSQR_ALGO):
+ *   TSQR_CQR2     CholeskyQR2: two CholeskyQR passes, R = R2 R1     (Alg. 3)
+ *   TSQR_CQR2GS   CholeskyQR2 with block Gram-Schmidt: two passes of the
+ *                 distributed CQRGS (Alg. 7), R = R2 R1
+ *   TSQR_MCQR2GS  the paper's modified CQR2GS (Alg. 8)
+ *   TSQR_CQR      single CholeskyQR pass (Alg. 2)        -- tests
+ *   TSQR_CQRGS    single CQRGS pass (Alg. 7)                         -- tests
+ *
+ * Conventions for every entry point:
+ *   - Matrices are FP64, COLUMN-MAJOR: element (r, c) of X is X[r + c*ldX].
+ *   - A and R passed to tsqr_factor are DEVICE pointers on the plan's device.
+ *   - All element offsets are 64-bit (m_local * n may exceed 2^31).
+ *   - Functions return a tsqr_status; they never abort the process.  A non-OK
+ *     status from tsqr_create leaves *plan == NULL.
+ *   - The library performs no host<->device copies of A or R, no cuBLAS/cuSOLVER
+ *     calls and has no CPU fallback: every arithmetic step runs in its own sm_100a
+ *     kernels.  Cross-GPU sums use NCCL allreduce (ncclFloat64, ncclSum).
+ *
+ * Citation keys: P:n = line n of the paper's LaTeX source;
+ * DESIGN.md lists the readings (R-k) taken where the paper is silent.
+ */
+#ifndef TSQR_H
+#define TSQR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tsqr_plan_s* tsqr_plan_t;
+
+typedef enum {
+  TSQR_OK = 0,
+  TSQR_ERR_INVALID_ARG = 1, /* bad pointer, size, leading dimension or alignment       */
+  TSQR_ERR_UNSUPPORTED = 2, /* valid but not supported in this version (see create)     */
+  TSQR_ERR_CUDA = 3,        /* a CUDA runtime call failed (message: tsqr_last_error)    */
+  TSQR_ERR_NCCL = 4,        /* an NCCL call failed or the communicator reported an error */
+  TSQR_ERR_BREAKDOWN = 5,   /* Cholesky breakdown: a Gram pivot <= 0 or non-finite      */
+  TSQR_ERR_WORKSPACE = 6    /* workspace NULL, too small or misaligned                   */
+} tsqr_status;
+
+typedef enum {
+  TSQR_CQR2 = 0,
+  TSQR_CQR2GS = 1,
+  TSQR_MCQR2GS = 2,
+  TSQR_CQR = 3,
+  TSQR_CQRGS = 4
+} tsqr_algo;
+
+/* Where a Cholesky breakdown happened (identical on every rank, since every rank
+ * factors the same allreduced Gram block).  pass: CQRGS pass (1 or 2; always 1 for
+ * the other methods); panel: 1-based panel index; stage: which CholeskyQR of that
+ * panel (1 = first, 2 = the second "re-orthogonalising" one of CQR2 / Alg. 8 l.8);
+ * pivot: 0-based column inside the panel's b x b Gram block; pivot_value: the
+ * offending pivot (<= 0, NaN or Inf).  Breakdown rule: unpivoted upper Cholesky
+ * W = U^T U fails iff a pivot d is not > 0 or not finite (R-5). */
+typedef struct {
+  int32_t pass, panel, stage, pivot;
+  double pivot_value;
+} tsqr_breakdown_info;
+
+/* Bytes of device workspace tsqr_create needs for this problem (0 on invalid
+ * arguments).  Depends only on (m_local, n, panel_b, nranks, algo). */
+size_t tsqr_workspace_bytes(int64_t m_local, int32_t n, int32_t panel_b, int32_t nranks,
+                            tsqr_algo algo);
+
+/* Create a plan.  COLLECTIVE over `nccl_comm` (every rank must call it with the
+ * same n, panel_b and algo; m_local may differ per rank).  When nccl_comm is NULL
+ * the plan is single-GPU (P = 1).
+ *   m_local        rows owned by this rank, >= 0 (sum over ranks >= n)
+ *   n              columns, 1 <= n <= 4096
+ *   panel_b        panel width b: required n % b == 0 and
+ *                  b in {16, 32, 64, 128, 256}; for CQR / CQR2, b must equal n and
+ *                  n <= 256 (single panel).  Ragged panels: TSQR_ERR_UNSUPPORTED.
+ *   nccl_comm      ncclComm_t (see tsqr_nccl_comm_init) or NULL
+ *   algo           method, see tsqr_algo
+ *   cuda_stream    cudaStream_t every launch and NCCL call is enqueued on (NULL =
+ *                  legacy default stream)
+ *   workspace      device buffer of >= tsqr_workspace_bytes(...) bytes, 256-byte
+ *                  aligned, owned by the caller and kept alive until destroy
+ * All ranks return the same status (arguments are validated with one small
+ * allreduce), so a bad argument on one rank cannot deadlock the others.
+ * The plan owns only host state; the caller owns A, R, workspace, stream, comm. */
+tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t panel_b,
+                        void* nccl_comm, tsqr_algo algo, void* cuda_stream, void* workspace,
+                        size_t workspace_bytes);
+
+/* Factor A = Q R.  COLLECTIVE; asynchronous on the plan's stream.
+ *   A    device, m_local x n, column-major, lda >= max(1, m_local); overwritten by
+ *        this rank's rows of Q.  8-byte aligned.
+ *   R    device, n x n, column-major, ldr >= n; receives the full upper triangle,
+ *        exact zeros strictly below the diagonal and a positive diagonal, bitwise
+ *        identical on all ranks.
+ * Returns TSQR_OK once everything is enqueued; numerical status (breakdown) is
+ * reported by tsqr_wait.  After a breakdown the contents of A and R are
+ * unspecified.  A plan is bound to one stream and is not thread-safe. */
+tsqr_status tsqr_factor(tsqr_plan_t plan, double* A, int64_t lda, double* R, int32_t ldr);
+
+/* Synchronise the plan's stream and return the sticky numerical status of the
+ * last tsqr_factor: TSQR_OK or TSQR_ERR_BREAKDOWN (details in *info, may be NULL),
+ * or TSQR_ERR_CUDA / TSQR_ERR_NCCL.  Reading the status is the only device->host
+ * transfer the library makes. */
+tsqr_status tsqr_wait(tsqr_plan_t plan, tsqr_breakdown_info* info);
+
+/* Number of allreduce calls and kernel launches the last tsqr_factor enqueued
+ * (4k-2 allreduces for CQR2GS and mCQR2GS, 2 for CQR2; Appendix A.2 of SURVEY).
+ * Either pointer may be NULL. */
+tsqr_status tsqr_last_counts(tsqr_plan_t plan, int64_t* allreduces, int64_t* launches);
+
+/* Destroy the plan (host state only). */
+tsqr_status tsqr_destroy(tsqr_plan_t plan);
+
+/* Human-readable name of a status; static storage. */
+const char* tsqr_status_string(tsqr_status s);
+
+/* Message of the last CUDA/NCCL error seen by this thread (static storage). */
+const char* tsqr_last_error(void);
+
+/* NCCL bootstrap.  tsqr_nccl_unique_id writes the 128-byte ncclUniqueId on rank 0;
+ * the caller broadcasts those bytes (e.g. over a torch.distributed group) and every
+ * rank calls tsqr_nccl_comm_init(&comm, nranks, rank, id, device).  The returned
+ * comm is owned by the caller and released with tsqr_nccl_comm_destroy. */
+tsqr_status tsqr_nccl_unique_id(void* id128);
+tsqr_status tsqr_nccl_comm_init(void** comm, int32_t nranks, int32_t rank, const void* id128,
+                                int32_t device);
+tsqr_status tsqr_nccl_comm_destroy(void* comm);
+
+/* ------------------------------------------------------------------------- */
+/* Step-level entry points (the hot-path steps of SURVEY §8(a), exposed so each */
+/* kernel can be checked against the oracle on its own).  All pointers device, */
+/* column-major, enqueued on `cuda_stream`, single GPU (no allreduce).          */
+/* ------------------------------------------------------------------------- */
+
+/* W (b x b, ldw >= b) = X^T X for X (m x b): the local Gram block (Alg. 2 l.2,
+ * P:152; Alg. 7 l.2), upper triangle computed with a fixed split-row
+ * partition and a fixed-order reduction, lower triangle mirrored bitwise (R-11).
+ * Deterministic.  b in {1..256}. */
+tsqr_status tsqr_gram(const double* X, int64_t ldx, int64_t m, int32_t b, double* W, int32_t ldw,
+                      void* cuda_stream);
+
+/* OUT (p x q, ldo >= p) = L^T Rm for L (m x p), Rm (m x q): the projection blocks
+ * Y = Q_j^T A_trail (Alg. 7 l.7; Alg. 8 l.3) and
+ * C = Q_{1:j-1}^T V (Alg. 8 l.7).  Deterministic. p, q <= 4096. */
+tsqr_status tsqr_proj(const double* L, int64_t ldl, const double* Rm, int64_t ldr, int64_t m,
+                      int32_t p, int32_t q, double* OUT, int32_t ldo, void* cuda_stream);
+
+/* X (m x q) -= L (m x p) * S (p x q), in place (Alg. 7 l.9; Alg. 8 l.4 and
+ * l.7).  p, q <= 4096. */
+tsqr_status tsqr_update(double* X, int64_t ldx, const double* L, int64_t ldl, const double* S,
+                        int32_t lds, int64_t m, int32_t p, int32_t q, void* cuda_stream);
+
+/* Cholesky W = U^T U (upper, unpivoted) and the explicit inverse Z = U^{-1}
+ * (Alg. 1 l.2; R-4, R-5).  W b x b (only the upper triangle is read);
+ * U and Z receive exact zeros below the diagonal.  On breakdown *status_dev
+ * (device int32[8]) is set to {1, pivot, ...} with the pivot value in
+ * status_dev[2..3] as a double; otherwise it is left untouched.  b <= 256. */
+tsqr_status tsqr_chol_inv(const double* W, int32_t ldw, int32_t b, double* U, int32_t ldu, double* Z,
+                          int32_t ldz, int32_t* status_dev, void* cuda_stream);
+
+/* X (m x b) <- X * Z in place for upper-triangular Z (b x b): panel
+ * orthogonalisation Q = A R^{-1} with the explicit inverse (Alg. 1 l.3, P:133;
+ * R-4).  b <= 256. */
+tsqr_status tsqr_trmm(double* X, int64_t ldx, int64_t m, int32_t b, const double* Z, int32_t ldz,
+                      void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSQR_H */

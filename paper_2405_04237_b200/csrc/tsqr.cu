@@ -1,0 +1,623 @@
+// tsqr.cu -- host orchestrator and C ABI of libtsqr (include/tsqr.h).
+//
+// The panel loops of the paper's algorithms (Alg. 2, 3, 7, 8 of arXiv 2405.04237) are
+// enqueued on one CUDA stream: every O(m) step is one of the sm_100a kernels in
+// kernels.cuh, every cross-GPU sum is one in-stream ncclAllReduce(ncclFloat64, ncclSum) of
+// a small replicated block (b x b Gram, b x N projection, (j-1)b x b re-orthogonalisation
+// block), and Cholesky / R assembly run redundantly on every rank.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "kernels.cuh"
+#include "tsqr.h"
+
+using namespace tsqr;
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+void set_err(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+#define CUDA_TRY(x)                                                                      \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess) {                                                             \
+      set_err("%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return TSQR_ERR_CUDA;                                                              \
+    }                                                                                    \
+  } while (0)
+
+#define NCCL_TRY(x)                                                                      \
+  do {                                                                                   \
+    ncclResult_t r_ = (x);                                                               \
+    if (r_ != ncclSuccess) {                                                             \
+      set_err("%s failed: %s (%s:%d)", #x, ncclGetErrorString(r_), __FILE__, __LINE__); \
+      return TSQR_ERR_NCCL;                                                              \
+    }                                                                                    \
+  } while (0)
+
+#define TRY(x)                          \
+  do {                                  \
+    tsqr_status s_ = (x);               \
+    if (s_ != TSQR_OK) return s_;       \
+  } while (0)
+
+constexpr int kSMs = 148;       // B200
+constexpr size_t kAlign = 256;
+
+size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+bool valid_b(int b) { return b == 16 || b == 32 || b == 64 || b == 128 || b == 256; }
+
+// ---- split-row policy of k_atb (a function of the problem only -> deterministic) ----
+struct AtbShape {
+  int ntp, ntq, tiles, S;
+  int64_t tps;  // row tiles per split
+};
+
+AtbShape atb_shape(int64_t m, int p, int q, bool gram) {
+  AtbShape s;
+  s.ntp = (p + 63) / 64;
+  s.ntq = (q + 63) / 64;
+  s.tiles = gram ? s.ntq * (s.ntq + 1) / 2 : s.ntp * s.ntq;
+  const int64_t ntr = (m + ATB_TR - 1) / ATB_TR;
+  int S = s.tiles >= kSMs ? 1 : kSMs / s.tiles;
+  const int64_t maxS = std::max<int64_t>(1, ntr / 4);  // >= 4 row tiles per split
+  if (S > maxS) S = (int)maxS;
+  if (S < 1) S = 1;
+  s.tps = std::max<int64_t>(1, (ntr + S - 1) / S);
+  s.S = (int)std::max<int64_t>(1, (ntr + s.tps - 1) / s.tps);
+  if (ntr == 0) s.S = 1;
+  return s;
+}
+
+size_t atb_part_doubles(int64_t m, int p, int q, bool gram) {
+  AtbShape s = atb_shape(m, p, q, gram);
+  return (size_t)s.S * (size_t)p * (size_t)q;
+}
+
+bool v16_ok(const void* ptr, int64_t ld) {
+  return ((reinterpret_cast<uintptr_t>(ptr) & 15u) == 0) && (ld % 2 == 0);
+}
+
+int grid_1d(int64_t n, int nt = 256) {
+  int64_t g = (n + nt - 1) / nt;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 4 * kSMs));
+}
+
+// ---- kernel launchers (single GPU, enqueue only) ----
+struct Launcher {
+  cudaStream_t st = nullptr;
+  int64_t launches = 0;
+  const int* status = nullptr;
+
+  tsqr_status atb(const double* L, int64_t ldl, const double* R, int64_t ldr, int64_t m, int p, int q, bool gram,
+                  double* part, double* out, int ldo) {
+    AtbShape sh = atb_shape(m, p, q, gram);
+    AtbArgs a{L, ldl, R, ldr, m, p, q, gram ? 1 : 0, sh.ntp, sh.ntq, sh.tps, part, status};
+    dim3 grid(sh.tiles, sh.S);
+    const bool v16 = v16_ok(L, ldl) && v16_ok(R, ldr);
+    if (v16) {
+      CUDA_TRY(cudaFuncSetAttribute(k_atb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ATB_SMEM));
+      k_atb<true><<<grid, NT, ATB_SMEM, st>>>(a);
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(k_atb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ATB_SMEM));
+      k_atb<false><<<grid, NT, ATB_SMEM, st>>>(a);
+    }
+    CUDA_TRY(cudaGetLastError());
+    k_reduce<<<grid_1d((int64_t)p * q), 256, 0, st>>>(part, sh.S, p, q, out, ldo, gram ? 1 : 0, status);
+    CUDA_TRY(cudaGetLastError());
+    launches += 2;
+    return TSQR_OK;
+  }
+
+  template <int B>
+  tsqr_status trmm_b(double* X, int64_t ldx, int64_t m, const double* Z, int ldz) {
+    using C = TrmmCfg<B>;
+    const int64_t ntr = (m + C::TR - 1) / C::TR;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntr, kSMs));
+    if (v16_ok(X, ldx)) {
+      CUDA_TRY(cudaFuncSetAttribute(k_trmm<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      k_trmm<B, true><<<grid, NT, C::SMEM, st>>>(X, ldx, m, Z, ldz, status);
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(k_trmm<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      k_trmm<B, false><<<grid, NT, C::SMEM, st>>>(X, ldx, m, Z, ldz, status);
+    }
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    return TSQR_OK;
+  }
+
+  tsqr_status trmm(double* X, int64_t ldx, int64_t m, int b, const double* Z, int ldz) {
+    switch (b) {
+      case 16: return trmm_b<16>(X, ldx, m, Z, ldz);
+      case 32: return trmm_b<32>(X, ldx, m, Z, ldz);
+      case 64: return trmm_b<64>(X, ldx, m, Z, ldz);
+      case 128: return trmm_b<128>(X, ldx, m, Z, ldz);
+      case 256: return trmm_b<256>(X, ldx, m, Z, ldz);
+      default: set_err("trmm: unsupported b=%d", b); return TSQR_ERR_UNSUPPORTED;
+    }
+  }
+
+  tsqr_status update(double* X, int64_t ldx, const double* L, int64_t ldl, const double* S, int64_t lds, int64_t m,
+                     int p, int q) {
+    UpdArgs a{X, ldx, L, ldl, S, lds, m, p, q, status};
+    const int64_t ntr = (m + UPD_TR - 1) / UPD_TR;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntr, kSMs));
+    if (v16_ok(L, ldl) && v16_ok(S, lds)) {
+      CUDA_TRY(cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UPD_SMEM));
+      k_update<true><<<grid, NT, UPD_SMEM, st>>>(a);
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(k_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UPD_SMEM));
+      k_update<false><<<grid, NT, UPD_SMEM, st>>>(a);
+    }
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    return TSQR_OK;
+  }
+
+  tsqr_status chol_inv(const double* W, int ldw, int b, double* U, int ldu, double* Z, int ldz, int* status_rw,
+                       int pass, int panel, int stage, double* work) {
+    const bool sm = b <= 128;
+    const size_t smem = sm ? sizeof(double) * (size_t)b * b : 0;
+    if (sm) CUDA_TRY(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_chol_inv<<<1, CHOL_NT, smem, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage, work, sm ? 1 : 0);
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    return TSQR_OK;
+  }
+
+  tsqr_status trimul(const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int n) {
+    k_trimul<<<grid_1d((int64_t)n * n), 256, 0, st>>>(A, lda, B, ldb, Cm, ldc, n, status);
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    return TSQR_OK;
+  }
+
+  tsqr_status gemm_acc_tri(const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int p, int q) {
+    k_gemm_acc_tri<<<grid_1d((int64_t)p * q), 256, 0, st>>>(A, lda, B, ldb, Cm, ldc, p, q, status);
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    return TSQR_OK;
+  }
+
+  tsqr_status copy2d(const double* S, int64_t lds, double* D, int64_t ldd, int rows, int cols) {
+    k_copy2d<<<grid_1d((int64_t)rows * cols), 256, 0, st>>>(S, lds, D, ldd, rows, cols, status);
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    return TSQR_OK;
+  }
+};
+
+}  // namespace
+
+// =========================================================================================
+// Plan
+// =========================================================================================
+struct tsqr_plan_s {
+  int64_t m = 0;        // local rows
+  int n = 0, b = 0, k = 0;
+  tsqr_algo algo = TSQR_CQR2;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  cudaStream_t stream = nullptr;
+  // workspace carve-up
+  int* status = nullptr;     // int32[16]
+  double* part = nullptr;    // split-row partials
+  double* W = nullptr;       // Gram block (b x b)
+  double* Y = nullptr;       // projection block (b x n) / (n x b)
+  double* U1 = nullptr;      // b x b
+  double* U2 = nullptr;      // b x b
+  double* Z = nullptr;       // b x b inverse
+  double* R1 = nullptr;      // n x n (CQR2GS pass 1 / CQR2 temporaries)
+  double* R2 = nullptr;      // n x n
+  double* cwork = nullptr;   // b x b Cholesky scratch for b > 128
+  Launcher L;
+  int64_t allreduces = 0;
+  tsqr_status sticky = TSQR_OK;
+};
+
+namespace {
+
+struct Carve {
+  size_t off = 0;
+  char* base = nullptr;
+  template <typename T>
+  T* take(size_t count) {
+    size_t at = align_up(off);
+    off = at + count * sizeof(T);
+    return base ? reinterpret_cast<T*>(base + at) : nullptr;
+  }
+};
+
+// Largest split-row partial buffer over every projection / Gram the algorithm issues.
+size_t max_part_doubles(int64_t m, int n, int b, tsqr_algo algo) {
+  size_t mx = atb_part_doubles(m, b, b, true);
+  const int k = n / b;
+  if (algo == TSQR_CQR2GS || algo == TSQR_CQRGS) {
+    for (int j = 0; j + 1 < k; ++j) mx = std::max(mx, atb_part_doubles(m, b, n - (j + 1) * b, false));
+  } else if (algo == TSQR_MCQR2GS) {
+    for (int j = 1; j < k; ++j) {
+      mx = std::max(mx, atb_part_doubles(m, b, n - j * b, false));
+      mx = std::max(mx, atb_part_doubles(m, j * b, b, false));
+    }
+  }
+  return mx;
+}
+
+size_t carve(Carve& c, tsqr_plan_s* p, int64_t m, int n, int b, tsqr_algo algo) {
+  int* status = c.take<int>(16);
+  double* part = c.take<double>(max_part_doubles(m, n, b, algo));
+  double* W = c.take<double>((size_t)b * b);
+  double* Y = c.take<double>((size_t)b * n);
+  double* U1 = c.take<double>((size_t)b * b);
+  double* U2 = c.take<double>((size_t)b * b);
+  double* Z = c.take<double>((size_t)b * b);
+  double* R1 = c.take<double>((size_t)n * n);
+  double* R2 = c.take<double>((size_t)n * n);
+  double* cw = c.take<double>((size_t)b * b);
+  if (p) {
+    p->status = status; p->part = part; p->W = W; p->Y = Y; p->U1 = U1; p->U2 = U2; p->Z = Z;
+    p->R1 = R1; p->R2 = R2; p->cwork = cw;
+  }
+  return align_up(c.off);
+}
+
+tsqr_status check_shape(int64_t m_local, int n, int b, tsqr_algo algo) {
+  if (m_local < 0 || n < 1 || n > 4096) { set_err("bad m_local/n"); return TSQR_ERR_INVALID_ARG; }
+  if (algo < TSQR_CQR2 || algo > TSQR_CQRGS) { set_err("bad algo"); return TSQR_ERR_INVALID_ARG; }
+  if (!valid_b(b)) { set_err("panel_b=%d not in {16,32,64,128,256}", b); return TSQR_ERR_UNSUPPORTED; }
+  if (n % b != 0) { set_err("ragged panels (n %% b != 0) unsupported"); return TSQR_ERR_UNSUPPORTED; }
+  if ((algo == TSQR_CQR2 || algo == TSQR_CQR) && b != n) { set_err("CQR/CQR2 need b == n"); return TSQR_ERR_INVALID_ARG; }
+  return TSQR_OK;
+}
+
+// ---- algorithm building blocks (plan-level, include the allreduce) ----
+tsqr_status allreduce(tsqr_plan_s* P, double* buf, size_t count) {
+  if (P->comm && P->nranks > 1) {
+    NCCL_TRY(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, P->comm, P->stream));
+    P->allreduces++;
+  } else {
+    P->allreduces++;  // counted: one Allreduce of the distributed algorithm (a no-op at P = 1)
+  }
+  return TSQR_OK;
+}
+
+// W <- allreduce(X^T X), X = m x w slab
+tsqr_status gram(tsqr_plan_s* P, const double* X, int64_t ldx, int w) {
+  TRY(P->L.atb(X, ldx, X, ldx, P->m, w, w, true, P->part, P->W, w));
+  return allreduce(P, P->W, (size_t)w * w);
+}
+
+// CholeskyQR of the m x w slab X in place (Alg. 2): U -> Uout (ldu), X <- X U^{-1}
+tsqr_status cqr(tsqr_plan_s* P, double* X, int64_t ldx, int w, double* Uout, int ldu, int pass, int panel, int stage) {
+  TRY(gram(P, X, ldx, w));
+  TRY(P->L.chol_inv(P->W, w, w, Uout, ldu, P->Z, w, P->status, pass, panel, stage, P->cwork));
+  return P->L.trmm(X, ldx, P->m, w, P->Z, w);
+}
+
+// OUT (p x q, ld p) <- allreduce(L^T Rm)
+tsqr_status proj(tsqr_plan_s* P, const double* Lm, int64_t ldl, int p, const double* Rm, int64_t ldr, int q, double* out) {
+  TRY(P->L.atb(Lm, ldl, Rm, ldr, P->m, p, q, false, P->part, out, p));
+  return allreduce(P, out, (size_t)p * q);
+}
+
+// one CQRGS pass (Alg. 7) writing its R into Rp (ld n)
+tsqr_status cqrgs_pass(tsqr_plan_s* P, double* A, int64_t lda, double* Rp, int ldr, int pass) {
+  const int n = P->n, b = P->b, k = P->k;
+  for (int j = 0; j < k; ++j) {
+    double* Aj = A + (int64_t)j * b * lda;
+    // R_jj = U (chol writes straight into R's diagonal block)
+    TRY(cqr(P, Aj, lda, b, Rp + (int64_t)j * b + (int64_t)j * b * ldr, ldr, pass, j + 1, 1));
+    const int nt = n - (j + 1) * b;
+    if (nt > 0) {
+      double* At = A + (int64_t)(j + 1) * b * lda;
+      TRY(proj(P, Aj, lda, b, At, lda, nt, P->Y));                            // l.7-8
+      TRY(P->L.update(At, lda, Aj, lda, P->Y, b, P->m, b, nt));               // l.9
+      TRY(P->L.copy2d(P->Y, b, Rp + (int64_t)j * b + (int64_t)(j + 1) * b * ldr, ldr, b, nt));  // l.10
+    }
+  }
+  return TSQR_OK;
+}
+
+tsqr_status run_mcqr2gs(tsqr_plan_s* P, double* A, int64_t lda, double* R, int ldr) {
+  const int n = P->n, b = P->b, k = P->k;
+  // l.1: CQR2 of panel 1
+  TRY(cqr(P, A, lda, b, P->U1, b, 1, 1, 1));
+  TRY(cqr(P, A, lda, b, P->U2, b, 1, 1, 2));
+  TRY(P->L.trimul(P->U2, b, P->U1, b, R, ldr, b));
+  for (int j = 1; j < k; ++j) {
+    double* Ap = A + (int64_t)(j - 1) * b * lda;  // Q_{j-1}
+    double* Aj = A + (int64_t)j * b * lda;
+    const int Nj = n - j * b;
+    // l.3-5: Y = Q_{j-1}^T A_{:,j:k}; A_{:,j:k} -= Q_{j-1} Y; R_{j-1,j:k} = Y
+    TRY(proj(P, Ap, lda, b, Aj, lda, Nj, P->Y));
+    TRY(P->L.update(Aj, lda, Ap, lda, P->Y, b, P->m, b, Nj));
+    TRY(P->L.copy2d(P->Y, b, R + (int64_t)(j - 1) * b + (int64_t)j * b * ldr, ldr, b, Nj));
+    // l.6: first CQR, panel -> V1, keep U1
+    TRY(cqr(P, Aj, lda, b, P->U1, b, 1, j + 1, 1));
+    // l.7: C = Q_{1:j-1}^T V1 ((j-1)b x b); V1 -= Q_{1:j-1} C
+    const int jb = j * b;
+    TRY(proj(P, A, lda, jb, Aj, lda, b, P->Y));
+    TRY(P->L.update(Aj, lda, A, lda, P->Y, jb, P->m, jb, b));
+    // l.8: second CQR -> Q_j, U2
+    TRY(cqr(P, Aj, lda, b, P->U2, b, 1, j + 1, 2));
+    // R_jj = U2 U1; R_{1:j-1,j} += C U1  (R-8)
+    TRY(P->L.trimul(P->U2, b, P->U1, b, R + (int64_t)jb + (int64_t)jb * ldr, ldr, b));
+    TRY(P->L.gemm_acc_tri(P->Y, jb, P->U1, b, R + (int64_t)jb * ldr, ldr, jb, b));
+  }
+  return TSQR_OK;
+}
+
+const char* status_names[] = {"TSQR_OK", "TSQR_ERR_INVALID_ARG", "TSQR_ERR_UNSUPPORTED", "TSQR_ERR_CUDA",
+                              "TSQR_ERR_NCCL", "TSQR_ERR_BREAKDOWN", "TSQR_ERR_WORKSPACE"};
+
+}  // namespace
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+extern "C" {
+
+const char* tsqr_status_string(tsqr_status s) {
+  if ((int)s < 0 || (int)s > 6) return "TSQR_UNKNOWN";
+  return status_names[(int)s];
+}
+
+const char* tsqr_last_error(void) { return g_err; }
+
+size_t tsqr_workspace_bytes(int64_t m_local, int32_t n, int32_t panel_b, int32_t nranks, tsqr_algo algo) {
+  (void)nranks;
+  if (check_shape(m_local, n, panel_b, algo) != TSQR_OK) return 0;
+  Carve c;
+  return carve(c, nullptr, m_local, n, panel_b, algo);
+}
+
+tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t panel_b, void* nccl_comm,
+                        tsqr_algo algo, void* cuda_stream, void* workspace, size_t workspace_bytes) {
+  if (!plan) { set_err("plan == NULL"); return TSQR_ERR_INVALID_ARG; }
+  *plan = nullptr;
+  tsqr_status st = check_shape(m_local, n, panel_b, algo);
+  size_t need = st == TSQR_OK ? tsqr_workspace_bytes(m_local, n, panel_b, 1, algo) : 0;
+  if (st == TSQR_OK && (!workspace || workspace_bytes < need || (reinterpret_cast<uintptr_t>(workspace) % kAlign))) {
+    set_err("workspace NULL, smaller than %zu bytes or not 256-byte aligned", need);
+    st = TSQR_ERR_WORKSPACE;
+  }
+  ncclComm_t comm = reinterpret_cast<ncclComm_t>(nccl_comm);
+  int nranks = 1, rank = 0;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  if (comm) {
+    NCCL_TRY(ncclCommCount(comm, &nranks));
+    NCCL_TRY(ncclCommUserRank(comm, &rank));
+    // collective argument validation: [n, b, algo, valid] min/max and sum(m_local)
+    int64_t h[6] = {n, panel_b, (int64_t)algo, st == TSQR_OK ? 1 : 0, m_local, 0};
+    int64_t* d = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), 3 * 6 * sizeof(int64_t), stream));
+    CUDA_TRY(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d + 6, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(d + 12, h, sizeof(h), cudaMemcpyHostToDevice, stream));
+    NCCL_TRY(ncclGroupStart());
+    NCCL_TRY(ncclAllReduce(d, d, 6, ncclInt64, ncclMin, comm, stream));
+    NCCL_TRY(ncclAllReduce(d + 6, d + 6, 6, ncclInt64, ncclMax, comm, stream));
+    NCCL_TRY(ncclAllReduce(d + 12, d + 12, 6, ncclInt64, ncclSum, comm, stream));
+    NCCL_TRY(ncclGroupEnd());
+    int64_t r[18];
+    CUDA_TRY(cudaMemcpyAsync(r, d, sizeof(r), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    CUDA_TRY(cudaFreeAsync(d, stream));
+    if (r[0] != r[6] || r[1] != r[7] || r[2] != r[8]) {
+      set_err("ranks disagree on n / panel_b / algo");
+      return TSQR_ERR_INVALID_ARG;
+    }
+    if (r[3] == 0) {
+      if (st == TSQR_OK) { set_err("another rank rejected its arguments"); st = TSQR_ERR_INVALID_ARG; }
+      return st;
+    }
+    if (r[12 + 4] < n) { set_err("global m < n"); return TSQR_ERR_INVALID_ARG; }
+  } else {
+    if (st != TSQR_OK) return st;
+    if (m_local < n) { set_err("m < n"); return TSQR_ERR_INVALID_ARG; }
+  }
+  if (st != TSQR_OK) return st;
+  tsqr_plan_s* p = new (std::nothrow) tsqr_plan_s();
+  if (!p) return TSQR_ERR_INVALID_ARG;
+  p->m = m_local; p->n = n; p->b = panel_b; p->k = n / panel_b; p->algo = algo;
+  p->comm = comm; p->nranks = nranks; p->rank = rank; p->stream = stream;
+  Carve c;
+  c.base = reinterpret_cast<char*>(workspace);
+  carve(c, p, m_local, n, panel_b, algo);
+  p->L.st = stream;
+  p->L.status = p->status;
+  *plan = p;
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_factor(tsqr_plan_t P, double* A, int64_t lda, double* R, int32_t ldr) {
+  if (!P) { set_err("plan == NULL"); return TSQR_ERR_INVALID_ARG; }
+  if ((!A && P->m > 0) || !R || lda < std::max<int64_t>(1, P->m) || ldr < P->n ||
+      (reinterpret_cast<uintptr_t>(A) & 7u) || (reinterpret_cast<uintptr_t>(R) & 7u)) {
+    set_err("bad A/R pointer or leading dimension");
+    return TSQR_ERR_INVALID_ARG;
+  }
+  P->L.launches = 0;
+  P->allreduces = 0;
+  P->sticky = TSQR_OK;
+  CUDA_TRY(cudaMemsetAsync(P->status, 0, 16 * sizeof(int), P->stream));
+  k_zero2d<<<grid_1d((int64_t)P->n * P->n), 256, 0, P->stream>>>(R, ldr, P->n, P->n);
+  CUDA_TRY(cudaGetLastError());
+  P->L.launches++;
+  const int n = P->n, b = P->b;
+  tsqr_status s = TSQR_OK;
+  switch (P->algo) {
+    case TSQR_CQR:
+      s = cqr(P, A, lda, n, R, ldr, 1, 1, 1);
+      break;
+    case TSQR_CQR2:
+      s = cqr(P, A, lda, n, P->U1, n, 1, 1, 1);
+      if (s == TSQR_OK) s = cqr(P, A, lda, n, P->U2, n, 1, 1, 2);
+      if (s == TSQR_OK) s = P->L.trimul(P->U2, n, P->U1, n, R, ldr, n);
+      break;
+    case TSQR_CQRGS:
+      s = cqrgs_pass(P, A, lda, R, ldr, 1);
+      break;
+    case TSQR_CQR2GS:
+      k_zero2d<<<grid_1d((int64_t)n * n), 256, 0, P->stream>>>(P->R1, n, n, n);
+      k_zero2d<<<grid_1d((int64_t)n * n), 256, 0, P->stream>>>(P->R2, n, n, n);
+      P->L.launches += 2;
+      s = cqrgs_pass(P, A, lda, P->R1, n, 1);
+      if (s == TSQR_OK) s = cqrgs_pass(P, A, lda, P->R2, n, 2);
+      if (s == TSQR_OK) s = P->L.trimul(P->R2, n, P->R1, n, R, ldr, n);
+      break;
+    case TSQR_MCQR2GS:
+      s = run_mcqr2gs(P, A, lda, R, ldr);
+      break;
+  }
+  (void)b;
+  P->sticky = s;
+  return s;
+}
+
+tsqr_status tsqr_wait(tsqr_plan_t P, tsqr_breakdown_info* info) {
+  if (!P) { set_err("plan == NULL"); return TSQR_ERR_INVALID_ARG; }
+  if (P->sticky != TSQR_OK) return P->sticky;
+  int h[16];
+  CUDA_TRY(cudaMemcpyAsync(h, P->status, sizeof(h), cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  if (P->comm) {
+    ncclResult_t async_err = ncclSuccess;
+    NCCL_TRY(ncclCommGetAsyncError(P->comm, &async_err));
+    if (async_err != ncclSuccess) { set_err("NCCL async error: %s", ncclGetErrorString(async_err)); return TSQR_ERR_NCCL; }
+  }
+  if (h[0] == 5) {
+    if (info) {
+      info->pass = h[1]; info->panel = h[2]; info->stage = h[3]; info->pivot = h[4];
+      double v;
+      std::memcpy(&v, &h[6], sizeof(double));
+      info->pivot_value = v;
+    }
+    return TSQR_ERR_BREAKDOWN;
+  }
+  if (info) std::memset(info, 0, sizeof(*info));
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_last_counts(tsqr_plan_t P, int64_t* allreduces, int64_t* launches) {
+  if (!P) return TSQR_ERR_INVALID_ARG;
+  if (allreduces) *allreduces = P->allreduces;
+  if (launches) *launches = P->L.launches;
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_destroy(tsqr_plan_t P) {
+  delete P;
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_nccl_unique_id(void* id128) {
+  if (!id128) return TSQR_ERR_INVALID_ARG;
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(id128, &id, sizeof(id));
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_nccl_comm_init(void** comm, int32_t nranks, int32_t rank, const void* id128, int32_t device) {
+  if (!comm || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return TSQR_ERR_INVALID_ARG;
+  CUDA_TRY(cudaSetDevice(device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclComm_t c = nullptr;
+  NCCL_TRY(ncclCommInitRank(&c, nranks, id, rank));
+  *comm = c;
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_nccl_comm_destroy(void* comm) {
+  if (!comm) return TSQR_OK;
+  NCCL_TRY(ncclCommDestroy(reinterpret_cast<ncclComm_t>(comm)));
+  return TSQR_OK;
+}
+
+// ---- step-level entry points (single GPU) ----
+namespace {
+struct Scratch {
+  double* part = nullptr;
+  size_t cap = 0;
+  ~Scratch() {}
+};
+thread_local Scratch g_scratch;
+
+tsqr_status scratch(size_t doubles, cudaStream_t st, double** out) {
+  if (g_scratch.cap < doubles) {
+    if (g_scratch.part) CUDA_TRY(cudaFreeAsync(g_scratch.part, st));
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&g_scratch.part), doubles * sizeof(double), st));
+    g_scratch.cap = doubles;
+  }
+  *out = g_scratch.part;
+  return TSQR_OK;
+}
+}  // namespace
+
+tsqr_status tsqr_gram(const double* X, int64_t ldx, int64_t m, int32_t b, double* W, int32_t ldw, void* cuda_stream) {
+  if (!W || (m > 0 && !X) || b < 1 || b > 4096 || ldx < std::max<int64_t>(1, m) || ldw < b) return TSQR_ERR_INVALID_ARG;
+  Launcher L;
+  L.st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  double* part;
+  TRY(scratch(atb_part_doubles(m, b, b, true), L.st, &part));
+  return L.atb(X, ldx, X, ldx, m, b, b, true, part, W, ldw);
+}
+
+tsqr_status tsqr_proj(const double* Lm, int64_t ldl, const double* Rm, int64_t ldr, int64_t m, int32_t p, int32_t q,
+                      double* OUT, int32_t ldo, void* cuda_stream) {
+  if (!OUT || (m > 0 && (!Lm || !Rm)) || p < 1 || q < 1 || p > 4096 || q > 4096 || ldl < std::max<int64_t>(1, m) ||
+      ldr < std::max<int64_t>(1, m) || ldo < p)
+    return TSQR_ERR_INVALID_ARG;
+  Launcher L;
+  L.st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  double* part;
+  TRY(scratch(atb_part_doubles(m, p, q, false), L.st, &part));
+  return L.atb(Lm, ldl, Rm, ldr, m, p, q, false, part, OUT, ldo);
+}
+
+tsqr_status tsqr_update(double* X, int64_t ldx, const double* Lm, int64_t ldl, const double* S, int32_t lds, int64_t m,
+                        int32_t p, int32_t q, void* cuda_stream) {
+  if ((m > 0 && (!X || !Lm)) || !S || p < 1 || q < 1 || p > 4096 || q > 4096 || ldx < std::max<int64_t>(1, m) ||
+      ldl < std::max<int64_t>(1, m) || lds < p)
+    return TSQR_ERR_INVALID_ARG;
+  Launcher L;
+  L.st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  return L.update(X, ldx, Lm, ldl, S, lds, m, p, q);
+}
+
+tsqr_status tsqr_chol_inv(const double* W, int32_t ldw, int32_t b, double* U, int32_t ldu, double* Z, int32_t ldz,
+                          int32_t* status_dev, void* cuda_stream) {
+  if (!W || !U || !Z || !status_dev || b < 1 || b > 256 || ldw < b || ldu < b || ldz < b) return TSQR_ERR_INVALID_ARG;
+  Launcher L;
+  L.st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  double* work = nullptr;
+  if (b > 128) TRY(scratch((size_t)b * b, L.st, &work));
+  return L.chol_inv(W, ldw, b, U, ldu, Z, ldz, status_dev, 1, 1, 1, work);
+}
+
+tsqr_status tsqr_trmm(double* X, int64_t ldx, int64_t m, int32_t b, const double* Z, int32_t ldz, void* cuda_stream) {
+  if ((m > 0 && !X) || !Z || ldx < std::max<int64_t>(1, m) || ldz < b) return TSQR_ERR_INVALID_ARG;
+  if (!valid_b(b)) return TSQR_ERR_UNSUPPORTED;
+  Launcher L;
+  L.st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  return L.trmm(X, ldx, m, b, Z, ldz);
+}
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+"""Whole-factorisation parity of the CUDA path (C ABI, single GPU) with the CPU oracle on
+the same seeded inputs, per the protocol of SURVEY §8(c) c6 / DESIGN.md §Parity:
+  1. both succeed and kappa <= 1e8: ||R_gpu - R_orc||_F / ||R_orc||_F <= 1e-10
+  2. mCQR2GS at every kappa in [1e2, 1e15]: ||Q^T Q - I||_F <= 1e-13, ||A - QR||_F/||A||_F <= 1e-14
+  3. CQR2 / CQR2GS: the same outcome class as the oracle (both pass the gate 2, or both fail /
+     break down).
+Plus invariants (exact zeros below diag(R), positive diagonal) and determinism. GPU only."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+KAPPAS = [10.0 ** e for e in range(2, 16)]
+
+
+@pytest.fixture(scope="module")
+def T():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2405_04237_b200 as t
+    t.load()
+    return t
+
+
+def run_gpu(T, A, b, algo):
+    Ad = T.to_colmajor(A)
+    try:
+        R = T.factor(Ad, b, algo)
+    except T.TsqrError as e:
+        if e.status == T.TSQR_ERR_BREAKDOWN:
+            return None, None, e.info
+        raise
+    return Ad.cpu().numpy(), R.cpu().numpy(), None
+
+
+def gates(orc, A, Q, R):
+    return orc.orthogonality(Q), orc.residual(A, Q, R)
+
+
+def check_invariants(R):
+    assert np.array_equal(np.tril(R, -1), np.zeros_like(R))
+    assert np.all(np.diag(R) > 0)
+
+
+@pytest.mark.parametrize("kappa", KAPPAS)
+def test_cfg1_mcqr2gs_sweep(T, orc, kappa):
+    """BASELINE configs[0]: m=4096, n=64, b=16, mCQR2GS, kappa sweep 1e2..1e15."""
+    A, _, _ = synth.generate_np(4096, 64, kappa, seed=0)
+    Qo, Ro, io = orc.factor(A, 16, "mcqr2gs")
+    Q, R, info = run_gpu(T, A, 16, "mcqr2gs")
+    assert io["status"] == 0 and info is None
+    check_invariants(R)
+    orth, res = gates(orc, A, Q, R)
+    assert orth <= 1e-13 and res <= 1e-14, (orth, res)
+    if kappa <= 1e8:
+        assert np.linalg.norm(R - Ro) / np.linalg.norm(Ro) <= 1e-10
+    if kappa <= 1e4:
+        assert np.linalg.norm(Q - Qo) / np.linalg.norm(Qo) <= 1e-11
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_cfg1_seeds(T, orc, seed):
+    A, _, _ = synth.generate_np(4096, 64, 1e8, seed=seed)
+    Qo, Ro, _ = orc.factor(A, 16, "mcqr2gs")
+    Q, R, info = run_gpu(T, A, 16, "mcqr2gs")
+    assert info is None
+    assert np.linalg.norm(R - Ro) / np.linalg.norm(Ro) <= 1e-10
+    orth, res = gates(orc, A, Q, R)
+    assert orth <= 1e-13 and res <= 1e-14
+
+
+def _outcome(orc, A, Q, R):
+    if Q is None:
+        return "breakdown", None
+    orth, res = gates(orc, A, Q, R)
+    return ("pass" if (orth <= 1e-13 and res <= 1e-14) else "fail"), orth
+
+
+def same_class(o_orc, o_gpu):
+    """Outcome-class parity (R-21): same class; or both completed with
+    orthogonality within 100x of each other (a value near the 1e-13 gate may land on
+    either side); or one broke down while the other lost orthogonality (> gate)."""
+    (co, vo), (cg, vg) = o_orc, o_gpu
+    if co == cg:
+        return True
+    if vo is not None and vg is not None:
+        return max(vo, vg) / min(vo, vg) <= 100.0
+    return {co, cg} == {"fail", "breakdown"}
+
+
+@pytest.mark.parametrize("algo,b", [("cqr2gs", 16), ("cqr2", 64), ("cqr2gs", 32)])
+@pytest.mark.parametrize("kappa", [1e2, 1e5, 1e8, 1e10, 1e12, 1e15])
+def test_cfg1_other_algorithms_outcome(T, orc, algo, b, kappa):
+    A, _, _ = synth.generate_np(4096, 64, kappa, seed=0)
+    Qo, Ro, io = orc.factor(A, b, algo)
+    Q, R, info = run_gpu(T, A, b, algo)
+    oo, og = _outcome(orc, A, Qo, Ro), _outcome(orc, A, Q, R)
+    if kappa <= 1e8:
+        assert oo[0] == og[0] == "pass"
+        assert np.linalg.norm(R - Ro) / np.linalg.norm(Ro) <= 1e-10
+    else:
+        assert same_class(oo, og), (oo, og)
+
+
+@pytest.mark.parametrize("m,n,b,kappa", [
+    (65536 + 37, 256, 64, 1e15),      # cfg2 shape class, ragged row tail
+    (65536 + 37, 256, 64, 1e6),
+    (2 ** 16 + 5, 512, 64, 1e15),     # cfg3 shape class
+    (2 ** 14 + 3, 1024, 128, 1e12),   # cfg4 panel widths
+    (2 ** 14 + 3, 1024, 256, 1e12),
+])
+def test_wide_mcqr2gs(T, orc, m, n, b, kappa):
+    A, _, _ = synth.generate_np(m, n, kappa, seed=0, chunk=m)
+    Qo, Ro, io = orc.factor(A, b, "mcqr2gs")
+    Q, R, info = run_gpu(T, A, b, "mcqr2gs")
+    assert io["status"] == 0 and info is None
+    check_invariants(R)
+    orth, res = gates(orc, A, Q, R)
+    assert orth <= 1e-13 and res <= 1e-14, (orth, res)
+    if kappa <= 1e8:
+        assert np.linalg.norm(R - Ro) / np.linalg.norm(Ro) <= 1e-10
+
+
+def test_cqr2_cfg5_shape(T, orc):
+    A, _, _ = synth.generate_np(2 ** 16 + 1, 128, 1e2, seed=0, chunk=2 ** 16 + 1)
+    Qo, Ro, _ = orc.factor(A, 128, "cqr2")
+    Q, R, info = run_gpu(T, A, 128, "cqr2")
+    assert info is None
+    check_invariants(R)
+    assert np.linalg.norm(R - Ro) / np.linalg.norm(Ro) <= 1e-10
+    orth, res = gates(orc, A, Q, R)
+    assert orth <= 1e-13 and res <= 1e-14
+
+
+def test_cqr2gs_cfg2_shape(T, orc):
+    """CQR2GS at kappa=1e15 with k=4: the GPU reproduces the oracle's outcome class."""
+    A, _, _ = synth.generate_np(65536, 256, 1e15, seed=0)
+    Qo, Ro, _ = orc.factor(A, 64, "cqr2gs")
+    Q, R, info = run_gpu(T, A, 64, "cqr2gs")
+    oo, og = _outcome(orc, A, Qo, Ro), _outcome(orc, A, Q, R)
+    assert same_class(oo, og), (oo, og)
+
+
+def test_degeneracies_gpu(T):
+    """k = 1: mCQR2GS and CQR2GS run exactly the CQR2 kernel sequence -> bitwise equal."""
+    A, _, _ = synth.generate_np(8192, 64, 1e6, seed=5)
+    Q2, R2, _ = run_gpu(T, A, 64, "cqr2")
+    for algo in ("mcqr2gs", "cqr2gs"):
+        Q, R, _ = run_gpu(T, A, 64, algo)
+        assert np.array_equal(Q, Q2) and np.array_equal(R, R2), algo
+
+
+def test_breakdown_reported_like_oracle(T, orc):
+    A, _, _ = synth.generate_np(4096, 64, 1e2, seed=15)
+    A[:, 20] = 0.0
+    _, _, io = orc.factor(A, 16, "mcqr2gs")
+    Q, R, info = run_gpu(T, A, 16, "mcqr2gs")
+    assert Q is None and io["status"] == 5
+    assert (info["pass"], info["panel"], info["stage"], info["pivot"]) == (io["pass"], io["panel"], io["stage"],
+                                                                          io["pivot"])
+
+
+def test_factor_deterministic_and_counts(T):
+    import torch
+    A, _, _ = synth.generate_np(65536, 256, 1e12, seed=6)
+    outs = []
+    for _ in range(2):
+        Ad = T.to_colmajor(A)
+        p = T.Plan(A.shape[0], 256, 64, "mcqr2gs")
+        R = p.factor(Ad)
+        outs.append((Ad.cpu().numpy(), R.cpu().numpy()))
+        ar, _ = p.counts()
+        assert ar == 4 * 4 - 2
+        p.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    torch.cuda.synchronize()
+
+
+def test_column_scaling_metamorphic_gpu(T):
+    """Power-of-two column scaling commutes with every rounded step of the GPU path too."""
+    A, _, _ = synth.generate_np(8192, 128, 1e12, seed=8)
+    D = np.ldexp(1.0, np.random.default_rng(0).integers(-5, 6, size=128))
+    Q1, R1, _ = run_gpu(T, A, 32, "mcqr2gs")
+    Q2, R2, _ = run_gpu(T, np.asfortranarray(A * D), 32, "mcqr2gs")
+    assert np.array_equal(Q1, Q2) and np.array_equal(R1 * D, R2)
