@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the distributed FP64 tall-and-skinny QR (arXiv 2405.04237) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+
+A "step" is one full factorisation A = QR of every rank's m_local x n block (all steps
+of the hot path: Gram, allreduce, Cholesky + inverse, TRMM, projections, updates, R
+assembly).  Between steps A is restored from a device copy A0 (untimed; 16 GiB per GPU
+at cfg3, far larger than the 126 MB L2, so no L2 flush is needed).  Each step is timed
+with CUDA events on the factorisation stream, bracketed by a barrier and a device
+synchronise on both sides; the step time is the max over ranks; value = total FP64
+flops of all ranks (4 m n^2, Appendix A.1 of SURVEY / Table 2 of the paper) / time.
+
+Default workload (BASELINE.json configs[2], the north-star target): modified CQR2-BGS,
+2^22 rows per GPU x 512 columns, panel width 64, kappa = 1e15, weak scaling.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "FP64 TFLOP/s + % roofline at 1/2/4/8 B200; ‖QᵀQ−I‖ at κ=1e15"
+CONFIGS = {
+    # name: (m_local, n, b, kappa, algo, description)
+    "cfg1": (4096, 64, 16, 1e8, "mcqr2gs", "BASELINE configs[0]: m=4096 n=64 b=16 kappa=1e8 mCQR2GS"),
+    "cfg2": (1 << 22, 256, 64, 1e15, "mcqr2gs", "BASELINE configs[1]: m=2^22 n=256 b=64 kappa=1e15 mCQR2GS"),
+    "cfg2-cqr2gs": (1 << 22, 256, 64, 1e15, "cqr2gs", "BASELINE configs[1]: m=2^22 n=256 b=64 kappa=1e15 CQR2GS"),
+    "cfg3": (1 << 22, 512, 64, 1e15, "mcqr2gs",
+             "BASELINE configs[2]: weak scaling 2^22 rows/GPU x n=512 b=64 kappa=1e15 mCQR2GS"),
+    "cfg4-128": (1 << 20, 2048, 128, 1e12, "mcqr2gs", "BASELINE configs[3]: 2^20 rows/GPU x n=2048 b=128 kappa=1e12"),
+    "cfg4-256": (1 << 20, 2048, 256, 1e12, "mcqr2gs", "BASELINE configs[3]: 2^20 rows/GPU x n=2048 b=256 kappa=1e12"),
+    "cfg5": (1 << 24, 128, 128, 1e2, "cqr2", "BASELINE configs[4]: CQR2 2^24 rows/GPU x n=128 kappa=1e2"),
+}
+
+
+def env_int(name, default):
+    v = os.environ.get(name)
+    return int(v) if v is not None and v != "" else default
+
+
+def flops_of(m_global: int, n: int) -> float:
+    """Algorithmic FP64 flops of one factorisation: 4 m n^2 (Table 2, Table 1;
+    identical for CQR2, CQR2GS and mCQR2GS up to terms < 1e-4 relative)."""
+    return 4.0 * m_global * n * n
+
+
+# ---------------------------------------------------------------------------- peaks
+def load_peaks():
+    peaks = {"fp64_tflops": 37.0, "fp64_tflops_sustained": 36.96, "hbm_gbs": 6538.6,
+             "fp64_source": "fallback", "hbm_source": "fallback"}
+    p = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        burst = max(v for k, v in d.items() if k.startswith("dmma_") and k.endswith("_tflops") and "sustained" not in k)
+        peaks.update(fp64_tflops=burst, fp64_tflops_sustained=d.get("dmma_m16n8k16_sustained_tflops", burst),
+                     fp64_source="measured: profiles/fp64_peaks_r01.json (DMMA loop on B200)")
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        d = json.load(open(mp))
+        if "hbm_gbs" in d:
+            peaks.update(hbm_gbs=float(d["hbm_gbs"]), hbm_source="measured: MEASURED_PEAKS.json")
+    return peaks
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.rows, self.proc, self.thread = [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+        return self.summary()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg):
+    """The oracle (plain C, all host cores) on a bounded row sample of the same workload."""
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    import synth
+    m_local, n, b, kappa, algo, desc = cfg
+    m_s = min(args.ref_rows, m_local * args.gpus)
+    A, _, _ = synth.generate_np(m_s, n, kappa, seed=0, chunk=min(m_s, 65536))
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        Q, R, info = oracle.factor(A, b, algo)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+        if info["status"] != 0:
+            break
+    total = sum(times)
+    value = flops_of(m_s, n) * len(times) / total / 1e12 if total > 0 else 0.0
+    sample = f"{m_s} x {n} rows (of {m_local * args.gpus} global), b={b}, kappa={kappa:g}, {algo}"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * total / max(1, len(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded A = U diag(sigma) V^T, P:108)",
+        "config": {"workload": desc, "m_local": m_local, "n": n, "b": b, "kappa": kappa, "algo": algo,
+                   "reference": "CPU oracle (oracle/oracle.c), bounded row sample"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "oracle_status": info["status"],
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(args, cfg):
+    import oracle
+    import synth
+    m_local, n, b, kappa, algo, desc = cfg
+    m_s = min(args.cpu_rows, m_local)
+    A, _, _ = synth.generate_np(m_s, n, kappa, seed=0, chunk=min(m_s, 65536))
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    t0 = time.perf_counter()
+    _, _, info = oracle.factor(A, b, algo)
+    dt = time.perf_counter() - t0
+    return {"value": flops_of(m_s, n) / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"one {algo} factorisation of {m_s} x {n} (b={b}, kappa={kappa:g}) on {cores} host threads, "
+                      f"{dt:.2f} s, status {info['status']}",
+            "seconds": dt}
+
+
+# ---------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-rows", type=int, default=1 << 16)
+    ap.add_argument("--cpu-rows", type=int, default=1 << 18)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--seed", type=int, default=0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2405_04237_b200 as tsqr
+    import synth
+    from harness import verify
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    comm = None
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+        comm = tsqr.NcclComm(rank, world, local)
+
+    m_local, n, b, kappa, algo, desc = cfg
+    m_global = m_local * world
+    peaks = load_peaks()
+
+    # ---- inputs: rows [rank*m_local, (rank+1)*m_local) of the global seeded test matrix
+    A = tsqr.colmajor_empty(m_local, n, device=dev)
+    synth.generate_torch(A, m_global, rank * m_local, n, kappa, seed=args.seed)
+    A0 = tsqr.colmajor_empty(m_local, n, device=dev)
+    A0.copy_(A)
+    R = tsqr.colmajor_empty(n, n, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    plan = tsqr.Plan(m_local, n, b, algo, comm=comm, stream=stream, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        A.copy_(A0)
+        plan.factor(A, R)
+    # ---- timed region: K steps, each bracketed by barrier + synchronize, device events
+    clocks = ClockSampler()
+    if rank == 0:
+        clocks.start()
+    plan.set_timing(True)
+    plan.timing_reset()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms = []
+    for _ in range(args.steps):
+        A.copy_(A0)
+        barrier()
+        e0.record(stream)
+        plan.factor(A, R, wait=False)
+        e1.record(stream)
+        plan.wait()
+        barrier()
+        step_ms.append(max_over_ranks(e0.elapsed_time(e1)))
+    clk = clocks.stop() if rank == 0 else None
+    kern = plan.timing()
+    plan.set_timing(False)
+    allreduces, launches = plan.counts()
+    total_ms = sum(step_ms)
+    value = flops_of(m_global, n) * args.steps / (total_ms / 1e3) / 1e12
+
+    # ---- accuracy of the last step (GPU verifier, chunked pairwise; harness/verify.py)
+    orth = verify.orthogonality(A, group=group)
+    res = verify.residual(A0, A, R, group=group)
+
+    # ---- roofline of the dominant kernel class (CUDA events inside the timed region)
+    ridge = peaks["fp64_tflops_sustained"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    heavy = {k: v for k, v in kern.items() if k in ("gram", "proj", "update", "trmm") and v["launches"]}
+    dom = max(heavy, key=lambda k: heavy[k]["ms"]) if heavy else None
+    roof = None
+    if dom:
+        d = kern[dom]
+        inten = d["flops"] / d["bytes"] if d["bytes"] else float("inf")
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(args.config, {}).get(dom)
+        if inten >= ridge:
+            ach = d["flops"] / (d["ms"] / 1e3) / 1e12
+            roof = {"bound": "tensor", "achieved": ach, "peak": peaks["fp64_tflops_sustained"], "unit": "TFLOP/s",
+                    "frac": ach / peaks["fp64_tflops_sustained"], "traffic": traffic}
+        else:
+            ach = d["bytes"] / (d["ms"] / 1e3) / 1e9
+            roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / peaks["hbm_gbs"], "traffic": traffic}
+        roof.update({"kernel": dom, "share_of_step": d["ms"] / total_ms,
+                     "per_launch": {"flops": d["flops"] / d["launches"], "bytes": d["bytes"] / d["launches"],
+                                    "ms": d["ms"] / d["launches"]},
+                     "dtype": "f64 (DMMA.8x8x4)", "peak_source": peaks["fp64_source"] if inten >= ridge else
+                     peaks["hbm_source"]})
+    breakdown = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                     "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] else None,
+                     "hbm_gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 and v["bytes"] else None}
+                 for k, v in kern.items()}
+
+    # ---- end to end through the C ABI with HOST buffers (tsqr_factor_host)
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty((n, m_local), dtype=torch.float64, pin_memory=True).T
+        Rh = torch.empty((n, n), dtype=torch.float64, pin_memory=True).T
+        e2e_ms = []
+        for _ in range(args.e2e_steps):
+            Ah.copy_(A0)           # untimed restore of the host input
+            barrier()
+            e0.record(stream)
+            plan.factor_host(Ah, Rh, A, R)
+            e1.record(stream)
+            plan.wait()
+            barrier()
+            e2e_ms.append(max_over_ranks(e0.elapsed_time(e1)))
+        del Ah
+        e2e = {"value": flops_of(m_global, n) * len(e2e_ms) / (sum(e2e_ms) / 1e3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": 8 * m_local * n * world, "d2h_bytes_per_step": (8 * m_local * n + 8 * n * n) * world,
+               "ms_per_step": sum(e2e_ms) / len(e2e_ms),
+               "api": "tsqr_factor_host: pinned host A -> device, factor, Q -> host A, R -> host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, cfg)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded A = U diag(sigma) V^T with log-spaced sigma, P:108)",
+            "config": {"workload": desc, "config": args.config, "m_local": m_local, "m_global": m_global, "n": n,
+                       "b": b, "kappa": kappa, "algo": algo, "parallelism": f"row-sharded dp{world} (NCCL allreduce)",
+                       "l2": "inputs 8*m_local*n bytes per GPU >> 126 MB L2; A restored from A0 between steps (untimed)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * args.steps,
+            "allreduces_per_step": allreduces,
+            "clocks": clk,
+            "rows_per_s": m_global * args.steps / (total_ms / 1e3),
+            "per_gpu_tflops": value / world,
+            "fp64_roofline_frac": value / world / peaks["fp64_tflops_sustained"],
+            "orthogonality": orth, "orthogonality_over_sqrt_n": orth / math.sqrt(n), "residual": res,
+            "step_ms": step_ms, "kernel_breakdown": breakdown, "peaks": peaks,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if comm:
+        torch.cuda.synchronize(dev)
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

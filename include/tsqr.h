@@ -118,6 +118,40 @@ tsqr_status tsqr_wait(tsqr_plan_t plan, tsqr_breakdown_info* info);
  * Either pointer may be NULL. */
 tsqr_status tsqr_last_counts(tsqr_plan_t plan, int64_t* allreduces, int64_t* launches);
 
+/* Factor from HOST buffers (the end-to-end form of tsqr_factor): A_host (m_local x n,
+ * ld lda_host) is copied to the caller's device buffer A_dev (ld lda_dev), factored in
+ * place, and Q is copied back over A_host; R is produced in R_dev (device, ldr_dev) and
+ * copied to R_host (ld ldr_host).  All copies are cudaMemcpy2DAsync on the plan's stream
+ * (asynchronous only if the host buffers are pinned, e.g. cudaHostAlloc / torch
+ * pin_memory).  COLLECTIVE like tsqr_factor; completes at tsqr_wait. */
+tsqr_status tsqr_factor_host(tsqr_plan_t plan, double* A_host, int64_t lda_host, double* R_host,
+                             int32_t ldr_host, double* A_dev, int64_t lda_dev, double* R_dev,
+                             int32_t ldr_dev);
+
+/* Per-kernel-class timing with CUDA events recorded on the plan's stream around every
+ * launch of the next tsqr_factor calls (off by default; enabling it adds two event
+ * records per launch).  Classes (TSQR_KCLASS_*): 0 Gram (split-row partials + reduce),
+ * 1 projection (Y, C), 2 trailing/re-orth update, 3 TRMM (Q = A U^{-1}), 4 Cholesky +
+ * inverse, 5 R assembly and other small kernels, 6 allreduce (NCCL).
+ * tsqr_timing synchronises the stream and returns, summed over every launch of `kclass`
+ * since the last tsqr_timing_reset: total milliseconds, launch count, and the
+ * ALGORITHMIC flops and HBM bytes of those launches (paper's flop counts: Gram m b^2,
+ * TRMM m b^2, projection / update 2 m p q; bytes = operands read + written once). */
+typedef enum {
+  TSQR_KCLASS_GRAM = 0,
+  TSQR_KCLASS_PROJ = 1,
+  TSQR_KCLASS_UPDATE = 2,
+  TSQR_KCLASS_TRMM = 3,
+  TSQR_KCLASS_CHOL = 4,
+  TSQR_KCLASS_SMALL = 5,
+  TSQR_KCLASS_ALLREDUCE = 6,
+  TSQR_KCLASS_COUNT = 7
+} tsqr_kclass;
+tsqr_status tsqr_set_timing(tsqr_plan_t plan, int32_t enable);
+tsqr_status tsqr_timing_reset(tsqr_plan_t plan);
+tsqr_status tsqr_timing(tsqr_plan_t plan, int32_t kclass, double* ms, int64_t* launches, double* flops,
+                        double* bytes);
+
 /* Destroy the plan (host state only). */
 tsqr_status tsqr_destroy(tsqr_plan_t plan);
 

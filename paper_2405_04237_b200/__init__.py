@@ -21,12 +21,13 @@ CQR2, CQR2GS, MCQR2GS, CQR, CQRGS = 0, 1, 2, 3, 4
 ALGOS = {"cqr2": CQR2, "cqr2gs": CQR2GS, "mcqr2gs": MCQR2GS, "cqr": CQR, "cqrgs": CQRGS}
 TSQR_OK, TSQR_ERR_INVALID_ARG, TSQR_ERR_UNSUPPORTED, TSQR_ERR_CUDA = 0, 1, 2, 3
 TSQR_ERR_NCCL, TSQR_ERR_BREAKDOWN, TSQR_ERR_WORKSPACE = 4, 5, 6
+KCLASSES = ["gram", "proj", "update", "trmm", "chol", "small", "allreduce"]
 
 LIB_PATH = _build.LIB
 
 #: every function declared in include/tsqr.h
 EXPORTS = ["tsqr_workspace_bytes", "tsqr_create", "tsqr_factor", "tsqr_wait", "tsqr_last_counts",
-           "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
+           "tsqr_factor_host", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
            "tsqr_nccl_comm_init", "tsqr_nccl_comm_destroy", "tsqr_gram", "tsqr_proj", "tsqr_update",
            "tsqr_chol_inv", "tsqr_trmm"]
 
@@ -69,6 +70,11 @@ def load(build_if_missing: bool = False):
     L.tsqr_wait.argtypes = [_VP, ctypes.POINTER(BreakdownInfo)]
     L.tsqr_last_counts.argtypes = [_VP, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]
     L.tsqr_destroy.argtypes = [_VP]
+    L.tsqr_factor_host.argtypes = [_VP, _VP, _I64, _VP, _I32, _VP, _I64, _VP, _I32]
+    L.tsqr_set_timing.argtypes = [_VP, _I32]
+    L.tsqr_timing_reset.argtypes = [_VP]
+    L.tsqr_timing.argtypes = [_VP, _I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
+                              ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
     L.tsqr_status_string.argtypes = [ctypes.c_int]
     L.tsqr_status_string.restype = ctypes.c_char_p
     L.tsqr_last_error.restype = ctypes.c_char_p
@@ -199,6 +205,29 @@ class Plan:
         info = BreakdownInfo()
         rc = L.tsqr_wait(self.handle, ctypes.byref(info))
         _check(rc, "tsqr_wait", info.as_dict() if rc == TSQR_ERR_BREAKDOWN else None)
+
+    def factor_host(self, A_host, R_host, A_dev, R_dev):
+        """End-to-end form: pinned host A (overwritten by Q) -> device -> factor -> host Q, R."""
+        L = load()
+        _check(L.tsqr_factor_host(self.handle, A_host.data_ptr(), _ld(A_host), R_host.data_ptr(), _ld(R_host),
+                                  A_dev.data_ptr(), _ld(A_dev), R_dev.data_ptr(), _ld(R_dev)), "tsqr_factor_host")
+
+    def set_timing(self, on: bool = True):
+        _check(load().tsqr_set_timing(self.handle, 1 if on else 0), "tsqr_set_timing")
+
+    def timing_reset(self):
+        _check(load().tsqr_timing_reset(self.handle), "tsqr_timing_reset")
+
+    def timing(self) -> dict:
+        """Per kernel class: {"ms", "launches", "flops", "bytes"} summed since timing_reset."""
+        L = load()
+        out = {}
+        for c, name in enumerate(KCLASSES):
+            ms, n, fl, by = ctypes.c_double(), _I64(), ctypes.c_double(), ctypes.c_double()
+            _check(L.tsqr_timing(self.handle, c, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl),
+                                 ctypes.byref(by)), "tsqr_timing")
+            out[name] = {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+        return out
 
     def counts(self) -> tuple[int, int]:
         L = load()

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "kernels.cuh"
 #include "tsqr.h"
@@ -98,17 +99,71 @@ int grid_1d(int64_t n, int nt = 256) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 4 * kSMs));
 }
 
+// ---- optional per-kernel-class event timing ----
+struct Timer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Rec { int cls; size_t e0, e1; double flops, bytes; };
+  std::vector<Rec> recs;
+  // accumulated totals per class (filled by harvest)
+  double ms[TSQR_KCLASS_COUNT] = {0}, fl[TSQR_KCLASS_COUNT] = {0}, by[TSQR_KCLASS_COUNT] = {0};
+  int64_t cnt[TSQR_KCLASS_COUNT] = {0};
+
+  size_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return (size_t)-1;
+      pool.push_back(e);
+    }
+    return used++;
+  }
+  size_t begin(cudaStream_t st) {
+    if (!on) return (size_t)-1;
+    size_t e = ev();
+    if (e != (size_t)-1) cudaEventRecord(pool[e], st);
+    return e;
+  }
+  void end(cudaStream_t st, size_t e0, int cls, double flops, double bytes) {
+    if (!on || e0 == (size_t)-1) return;
+    size_t e1 = ev();
+    if (e1 == (size_t)-1) return;
+    cudaEventRecord(pool[e1], st);
+    recs.push_back({cls, e0, e1, flops, bytes});
+  }
+  // fold recorded events into the totals (events must be complete)
+  void harvest() {
+    for (const Rec& r : recs) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, pool[r.e0], pool[r.e1]);
+      ms[r.cls] += t; fl[r.cls] += r.flops; by[r.cls] += r.bytes; cnt[r.cls] += 1;
+    }
+    recs.clear();
+    used = 0;
+  }
+  void reset() {
+    recs.clear(); used = 0;
+    for (int c = 0; c < TSQR_KCLASS_COUNT; ++c) { ms[c] = fl[c] = by[c] = 0; cnt[c] = 0; }
+  }
+  ~Timer() { for (auto e : pool) cudaEventDestroy(e); }
+};
+
 // ---- kernel launchers (single GPU, enqueue only) ----
 struct Launcher {
   cudaStream_t st = nullptr;
   int64_t launches = 0;
   const int* status = nullptr;
+  Timer* timer = nullptr;
+
+  size_t tbegin() { return timer ? timer->begin(st) : (size_t)-1; }
+  void tend(size_t e0, int cls, double flops, double bytes) { if (timer) timer->end(st, e0, cls, flops, bytes); }
 
   tsqr_status atb(const double* L, int64_t ldl, const double* R, int64_t ldr, int64_t m, int p, int q, bool gram,
                   double* part, double* out, int ldo) {
     AtbShape sh = atb_shape(m, p, q, gram);
     AtbArgs a{L, ldl, R, ldr, m, p, q, gram ? 1 : 0, sh.ntp, sh.ntq, sh.tps, part, status};
     dim3 grid(sh.tiles, sh.S);
+    const size_t t0 = tbegin();
     const bool v16 = v16_ok(L, ldl) && v16_ok(R, ldr);
     if (v16) {
       CUDA_TRY(cudaFuncSetAttribute(k_atb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ATB_SMEM));
@@ -121,6 +176,8 @@ struct Launcher {
     k_reduce<<<grid_1d((int64_t)p * q), 256, 0, st>>>(part, sh.S, p, q, out, ldo, gram ? 1 : 0, status);
     CUDA_TRY(cudaGetLastError());
     launches += 2;
+    if (gram) tend(t0, TSQR_KCLASS_GRAM, (double)m * p * p, 8.0 * m * p);
+    else tend(t0, TSQR_KCLASS_PROJ, 2.0 * m * p * q, 8.0 * m * (p + q));
     return TSQR_OK;
   }
 
@@ -129,6 +186,7 @@ struct Launcher {
     using C = TrmmCfg<B>;
     const int64_t ntr = (m + C::TR - 1) / C::TR;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntr, kSMs));
+    const size_t t0 = tbegin();
     if (v16_ok(X, ldx)) {
       CUDA_TRY(cudaFuncSetAttribute(k_trmm<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
       k_trmm<B, true><<<grid, NT, C::SMEM, st>>>(X, ldx, m, Z, ldz, status);
@@ -138,6 +196,7 @@ struct Launcher {
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
+    tend(t0, TSQR_KCLASS_TRMM, (double)m * B * B, 16.0 * m * B);
     return TSQR_OK;
   }
 
@@ -157,6 +216,7 @@ struct Launcher {
     UpdArgs a{X, ldx, L, ldl, S, lds, m, p, q, status};
     const int64_t ntr = (m + UPD_TR - 1) / UPD_TR;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntr, kSMs));
+    const size_t t0 = tbegin();
     if (v16_ok(L, ldl) && v16_ok(S, lds)) {
       CUDA_TRY(cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UPD_SMEM));
       k_update<true><<<grid, NT, UPD_SMEM, st>>>(a);
@@ -166,6 +226,7 @@ struct Launcher {
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
+    tend(t0, TSQR_KCLASS_UPDATE, 2.0 * m * p * q, 8.0 * m * (p + 2.0 * q));
     return TSQR_OK;
   }
 
@@ -174,30 +235,38 @@ struct Launcher {
     const bool sm = b <= 128;
     const size_t smem = sm ? sizeof(double) * (size_t)b * b : 0;
     if (sm) CUDA_TRY(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t t0 = tbegin();
     k_chol_inv<<<1, CHOL_NT, smem, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage, work, sm ? 1 : 0);
     CUDA_TRY(cudaGetLastError());
     launches += 1;
+    tend(t0, TSQR_KCLASS_CHOL, (double)b * b * b / 3.0 + (double)b * b * b / 3.0, 16.0 * b * b);
     return TSQR_OK;
   }
 
   tsqr_status trimul(const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int n) {
+    const size_t t0 = tbegin();
     k_trimul<<<grid_1d((int64_t)n * n), 256, 0, st>>>(A, lda, B, ldb, Cm, ldc, n, status);
     CUDA_TRY(cudaGetLastError());
     launches += 1;
+    tend(t0, TSQR_KCLASS_SMALL, 0.0, 0.0);
     return TSQR_OK;
   }
 
   tsqr_status gemm_acc_tri(const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int p, int q) {
+    const size_t t0 = tbegin();
     k_gemm_acc_tri<<<grid_1d((int64_t)p * q), 256, 0, st>>>(A, lda, B, ldb, Cm, ldc, p, q, status);
     CUDA_TRY(cudaGetLastError());
     launches += 1;
+    tend(t0, TSQR_KCLASS_SMALL, 0.0, 0.0);
     return TSQR_OK;
   }
 
   tsqr_status copy2d(const double* S, int64_t lds, double* D, int64_t ldd, int rows, int cols) {
+    const size_t t0 = tbegin();
     k_copy2d<<<grid_1d((int64_t)rows * cols), 256, 0, st>>>(S, lds, D, ldd, rows, cols, status);
     CUDA_TRY(cudaGetLastError());
     launches += 1;
+    tend(t0, TSQR_KCLASS_SMALL, 0.0, 0.0);
     return TSQR_OK;
   }
 };
@@ -226,6 +295,7 @@ struct tsqr_plan_s {
   double* R2 = nullptr;      // n x n
   double* cwork = nullptr;   // b x b Cholesky scratch for b > 128
   Launcher L;
+  Timer timer;
   int64_t allreduces = 0;
   tsqr_status sticky = TSQR_OK;
 };
@@ -288,7 +358,9 @@ tsqr_status check_shape(int64_t m_local, int n, int b, tsqr_algo algo) {
 // ---- algorithm building blocks (plan-level, include the allreduce) ----
 tsqr_status allreduce(tsqr_plan_s* P, double* buf, size_t count) {
   if (P->comm && P->nranks > 1) {
+    const size_t t0 = P->L.tbegin();
     NCCL_TRY(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, P->comm, P->stream));
+    P->L.tend(t0, TSQR_KCLASS_ALLREDUCE, 0.0, 8.0 * count);
     P->allreduces++;
   } else {
     P->allreduces++;  // counted: one Allreduce of the distributed algorithm (a no-op at P = 1)
@@ -441,6 +513,7 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
   carve(c, p, m_local, n, panel_b, algo);
   p->L.st = stream;
   p->L.status = p->status;
+  p->L.timer = &p->timer;
   *plan = p;
   return TSQR_OK;
 }
@@ -518,6 +591,50 @@ tsqr_status tsqr_last_counts(tsqr_plan_t P, int64_t* allreduces, int64_t* launch
   if (!P) return TSQR_ERR_INVALID_ARG;
   if (allreduces) *allreduces = P->allreduces;
   if (launches) *launches = P->L.launches;
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_factor_host(tsqr_plan_t P, double* A_host, int64_t lda_host, double* R_host, int32_t ldr_host,
+                             double* A_dev, int64_t lda_dev, double* R_dev, int32_t ldr_dev) {
+  if (!P || (P->m > 0 && (!A_host || !A_dev)) || !R_host || !R_dev || lda_host < std::max<int64_t>(1, P->m) ||
+      ldr_host < P->n) {
+    set_err("bad host/device buffers");
+    return TSQR_ERR_INVALID_ARG;
+  }
+  const size_t rowb = sizeof(double) * (size_t)P->m;
+  if (P->m > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(A_dev, sizeof(double) * lda_dev, A_host, sizeof(double) * lda_host, rowb, P->n,
+                               cudaMemcpyHostToDevice, P->stream));
+  TRY(tsqr_factor(P, A_dev, lda_dev, R_dev, ldr_dev));
+  if (P->m > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(A_host, sizeof(double) * lda_host, A_dev, sizeof(double) * lda_dev, rowb, P->n,
+                               cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaMemcpy2DAsync(R_host, sizeof(double) * ldr_host, R_dev, sizeof(double) * ldr_dev,
+                             sizeof(double) * P->n, P->n, cudaMemcpyDeviceToHost, P->stream));
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_set_timing(tsqr_plan_t P, int32_t enable) {
+  if (!P) return TSQR_ERR_INVALID_ARG;
+  P->timer.on = enable != 0;
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_timing_reset(tsqr_plan_t P) {
+  if (!P) return TSQR_ERR_INVALID_ARG;
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->timer.reset();
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_timing(tsqr_plan_t P, int32_t kclass, double* ms, int64_t* launches, double* flops, double* bytes) {
+  if (!P || kclass < 0 || kclass >= TSQR_KCLASS_COUNT) return TSQR_ERR_INVALID_ARG;
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->timer.harvest();
+  if (ms) *ms = P->timer.ms[kclass];
+  if (launches) *launches = P->timer.cnt[kclass];
+  if (flops) *flops = P->timer.fl[kclass];
+  if (bytes) *bytes = P->timer.by[kclass];
   return TSQR_OK;
 }
 
