@@ -1,0 +1,609 @@
+// stream_kernels.cuh -- the O(m) streaming kernels of the hot path:
+// split-row projections / Gram (k_proj), in-place trailing and re-orthogonalisation
+// updates (k_update) and in-place panel orthogonalisation (k_trmm).
+//
+// All three are persistent, warp-specialised CTAs: one producer warp streams tiles of the
+// tall operands into a ring of shared-memory stages with 2-D TMA tensor copies -- ONE
+// cp.async.bulk.tensor per 64-column tile, box = (TR + 4) rows x 64 columns, so the tile
+// lands column by column with the padded leading dimension LDT = TR + 4 == 4 (mod 16) that
+// makes every DMMA fragment load bank-conflict free; the 4 extra rows are never read, rows
+// past m and columns past the operand are zero-filled by the TMA unit.  Each stage has a
+// "full" mbarrier (arrive.expect_tx + complete_tx) and an "empty" mbarrier released by the
+// eight consumer warps, which run DMMA.8x8x4 contractions.  No CTA-wide barrier sits on the
+// streaming path.  Odd leading dimensions (no 16-byte TMA strides) fall back to a cp.async
+// producer with the same pipeline.
+#pragma once
+#include "common.cuh"
+
+namespace tsqr {
+
+constexpr int TR = 64;                // rows per streamed tile
+constexpr int LDT = TR + 4;           // padded leading dimension (== 4 mod 16) = TMA box rows
+constexpr int TILE = 64 * LDT;        // doubles in one 64-column tile
+constexpr uint32_t TILE_BYTES = TILE * 8;
+
+// smem base rounded up to 128 bytes (TMA destinations); callers request +128 bytes
+__device__ __forceinline__ double* aligned_smem(double* p) {
+  return reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+}
+
+// =========================================================================================
+// k_proj: PART[s] (p x q, ld p) = sum over the rows of split s of L^T Rm.
+//   gram = 1: L == Rm, upper 64x64 output tiles only; diagonal tiles use the DIAG schedule
+//   (diag_half: the A and B fragments of X^T X coincide, 8 fragment loads feed 18 DMMAs).
+//   Other tiles: FULL schedule, 2 k-halves x 2x2 warp tiles of 32x32.
+// grid = (#output tiles, S splits); the warps' partials are combined in a fixed order.
+// (Alg. 2 l.2 P:152, Alg. 7 l.2/l.7 P:344/Alg. 8 l.3/l.7 P:464/P:468)
+// =========================================================================================
+constexpr int PROJ_NS = 3;
+constexpr size_t PROJ_SMEM = sizeof(double) * (size_t)PROJ_NS * 2 * TILE + 2 * PROJ_NS * sizeof(uint64_t) + 128;
+
+struct ProjArgs {
+  CUtensorMap mapL;  // L: rows m, cols p   (TMA path)
+  CUtensorMap mapR;  // Rm: rows m, cols q
+  const double* L;
+  int64_t ldl;
+  const double* R;
+  int64_t ldr;
+  int64_t m;
+  int p, q;
+  int gram;
+  int ntp, ntq;
+  int64_t tiles_per_split;
+  double* part;  // [S][p*q]
+  const int* status;
+};
+
+// DIAG schedule of a diagonal Gram tile: warp group H (= warp / 4) owns the upper 8x8 blocks
+// t in [18H, 18H+18) (column-major block order), warp wq = warp % 4 owns rows [16wq, 16wq+16)
+// of every staged tile (4 k-steps): 36 accumulators per lane, 8 fragment loads per 18 DMMAs.
+template <int H>
+__device__ __forceinline__ void diag_half(const double* sL, int wq, int gid, int tig, double (&acc)[36]) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k0 = wq * 16 + ks * 4 + tig;
+    double f[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) f[c] = sL[(c * 8 + gid) * LDT + k0];
+    int t = 0;
+#pragma unroll
+    for (int bj = 0; bj < 8; ++bj)
+#pragma unroll
+      for (int bi = 0; bi <= bj; ++bi) {
+        if (t >= 18 * H && t < 18 * H + 18) dmma(acc[2 * (t - 18 * H)], acc[2 * (t - 18 * H) + 1], f[bi], f[bj]);
+        ++t;
+      }
+  }
+}
+
+template <bool TMA>
+__global__ void __launch_bounds__(NTHR, 1) k_proj(const __grid_constant__ ProjArgs a) {
+  extern __shared__ __align__(128) double smem_raw[];
+  if (failed(a.status)) return;
+  double* smem = aligned_smem(smem_raw);
+  double* bufL = smem;
+  double* bufR = smem + PROJ_NS * TILE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * PROJ_NS * TILE);
+  uint64_t* empty = full + PROJ_NS;
+
+  int ti, tj;
+  if (a.gram) {
+    int bx = blockIdx.x, j = 0;
+    while (bx > j) { bx -= j + 1; ++j; }
+    ti = bx; tj = j;
+  } else {
+    ti = blockIdx.x % a.ntp;
+    tj = blockIdx.x / a.ntp;
+  }
+  const bool diag = a.gram && ti == tj;
+  const int s = blockIdx.y;
+  const int64_t ntr = (a.m + TR - 1) / TR;
+  const int64_t t0 = (int64_t)s * a.tiles_per_split;
+  const int64_t t1 = min(ntr, t0 + a.tiles_per_split);
+  const int nt = (int)(t1 > t0 ? t1 - t0 : 0);
+  const int pc0 = ti * 64, qc0 = tj * 64;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PROJ_NS; ++i) {
+      mbar_init(&full[i], TMA ? 1 : 32);
+      mbar_init(&empty[i], NCW);
+    }
+    if (TMA) {
+      tma_prefetch_map(&a.mapL);
+      if (!diag) tma_prefetch_map(&a.mapR);
+    }
+  }
+  __syncthreads();
+
+  if (warp == PRODUCER) {
+    for (int it = 0; it < nt; ++it) {
+      const int st = it % PROJ_NS, use = it / PROJ_NS;
+      if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
+      const int64_t row0 = (t0 + it) * TR;
+      if (TMA) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[st], diag ? TILE_BYTES : 2 * TILE_BYTES);
+          tma_load_2d(bufL + st * TILE, &a.mapL, (int)row0, pc0, &full[st]);
+          if (!diag) tma_load_2d(bufR + st * TILE, &a.mapR, (int)row0, qc0, &full[st]);
+        }
+      } else {
+        produce_tile<TR, LDT, false, 64>(bufL + st * TILE, a.L, a.ldl, row0, a.m, pc0, a.p, lane);
+        if (!diag) produce_tile<TR, LDT, false, 64>(bufR + st * TILE, a.R, a.ldr, row0, a.m, qc0, a.q, lane);
+        cp_async_arrive(&full[st]);
+      }
+    }
+    return;
+  }
+
+  const int gid = lane >> 2, tig = lane & 3;
+  double acc[36];
+#pragma unroll
+  for (int i = 0; i < 36; ++i) acc[i] = 0.0;
+
+  for (int it = 0; it < nt; ++it) {
+    const int st = it % PROJ_NS;
+    mbar_wait(&full[st], (it / PROJ_NS) & 1);
+    const double* sL = bufL + st * TILE;
+    if (diag) {
+      if (warp < 4) diag_half<0>(sL, warp & 3, gid, tig, acc);
+      else diag_half<1>(sL, warp & 3, gid, tig, acc);
+    } else {
+      const double* sR = bufR + st * TILE;
+      const int h = warp >> 2, wi = (warp >> 1) & 1, wj = warp & 1;
+#pragma unroll 2
+      for (int ks = 0; ks < 8; ++ks) {
+        const int k0 = h * 32 + ks * 4 + tig;
+        double fa[4], fb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) fa[i] = sL[(wi * 32 + i * 8 + gid) * LDT + k0];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) fb[j] = sR[(wj * 32 + j * 8 + gid) * LDT + k0];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[2 * (i * 4 + j)], acc[2 * (i * 4 + j) + 1], fa[i], fb[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+
+  // every staged tile has been consumed -> the ring can be reused for the warp partials
+  consumer_sync();
+  double* red = smem;
+  double* outp = a.part + (int64_t)s * a.p * a.q;
+  if (diag) {
+#pragma unroll
+    for (int u = 0; u < 18; ++u) {
+      red[warp * 1152 + u * 64 + lane * 2] = acc[2 * u];
+      red[warp * 1152 + u * 64 + lane * 2 + 1] = acc[2 * u + 1];
+    }
+    consumer_sync();
+    for (int e = threadIdx.x; e < 2304; e += NCW * 32) {
+      const int t = e >> 6, H = t / 18, u = t - 18 * H, off = u * 64 + (e & 63);
+      const double* base = red + H * 4 * 1152 + off;
+      const double v = (base[0] + base[1152]) + (base[2 * 1152] + base[3 * 1152]);
+      int bi, bj;
+      upper_block(t, bi, bj);
+      const int ln = (e & 63) >> 1, hi = e & 1;
+      const int r = bi * 8 + (ln >> 2), c = bj * 8 + 2 * (ln & 3) + hi;
+      const int gr = pc0 + r, gc = qc0 + c;
+      if (gr < a.p && gc < a.q && r <= c) outp[gr + (int64_t)gc * a.p] = v;
+    }
+  } else {
+    const int h = warp >> 2, wi = (warp >> 1) & 1, wj = warp & 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = wi * 32 + i * 8 + gid, c = wj * 32 + j * 8 + 2 * tig;
+        red[h * 4096 + c * 64 + r] = acc[2 * (i * 4 + j)];
+        red[h * 4096 + (c + 1) * 64 + r] = acc[2 * (i * 4 + j) + 1];
+      }
+    consumer_sync();
+    for (int e = threadIdx.x; e < 4096; e += NCW * 32) {
+      const int r = e & 63, c = e >> 6;
+      const double v = red[e] + red[4096 + e];
+      const int gr = pc0 + r, gc = qc0 + c;
+      if (gr < a.p && gc < a.q && (!a.gram || gr <= gc)) outp[gr + (int64_t)gc * a.p] = v;
+    }
+  }
+}
+
+// =========================================================================================
+// k_update: X (m x q) -= L (m x p) * S (p x q), in place (Alg. 7 l.9 P:351; Alg. 8 l.4
+// P:465 and l.7 P:468).  Work units (row tile, 64-column chunk xc of X, 64-wide k-chunk kc)
+// in order kc < xc < tile; each operand lives in its own 2-slot ring and is re-staged only
+// when it changes (L once per row tile when p <= 64, S once per CTA when p, q <= 64, X once
+// per (tile, xc)).  Consumer warp tile: 32 rows x 16 columns (2 x 4 warp grid); the
+// accumulators hold -X so that -X + L S needs no negation in the inner loop.
+// Optional fused epilogue (gram_part != nullptr, q >= 64): the Gram of the updated first 64
+// columns (the next panel to be factored) accumulated per CTA into gram_part[blockIdx.x]
+// (64x64, upper blocks) -- the panel is not re-read for its CholeskyQR.
+// =========================================================================================
+constexpr size_t UPD_SMEM = sizeof(double) * (size_t)6 * TILE + 12 * sizeof(uint64_t) + 128;
+
+struct UpdArgs {
+  CUtensorMap mapX;  // X: rows m, cols q
+  CUtensorMap mapL;  // L: rows m, cols p
+  CUtensorMap mapS;  // S: rows p, cols q
+  double* X;
+  int64_t ldx;
+  const double* L;
+  int64_t ldl;
+  const double* S;
+  int64_t lds;
+  int64_t m;
+  int p, q;
+  double* gram_part;  // [gridDim.x][64*64] or nullptr
+  const int* status;
+};
+
+template <bool TMA>
+__global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdArgs a) {
+  extern __shared__ __align__(128) double smem_raw[];
+  if (failed(a.status)) return;
+  double* smem = aligned_smem(smem_raw);
+  double* ringL = smem;             // 2 slots
+  double* ringS = smem + 2 * TILE;  // 2 slots
+  double* ringX = smem + 4 * TILE;  // 2 slots
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * TILE);
+  uint64_t *fullL = bars, *emptyL = bars + 2, *fullS = bars + 4, *emptyS = bars + 6, *fullX = bars + 8,
+           *emptyX = bars + 10;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntr = (a.m + TR - 1) / TR;
+  const int nxc = (a.q + 63) / 64, nkc = (a.p + 63) / 64;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int nmine = (int)(first < ntr ? (ntr - 1 - first) / stride + 1 : 0);
+  const int units = nmine * nxc * nkc;
+  const bool fuse_gram = a.gram_part != nullptr;
+  // which operands change at unit u (same rule on both sides)
+  auto newL = [&](int u) { return nkc > 1 || (u % nxc) == 0; };  // nkc == 1: new row tile
+  auto newS = [&](int u) { return (nkc > 1 || nxc > 1) || u == 0; };
+  auto newX = [&](int u) { return (u % nkc) == 0; };
+
+  if (threadIdx.x == 0) {
+    const uint32_t fc = TMA ? 1 : 32;
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&fullL[i], fc); mbar_init(&emptyL[i], NCW);
+      mbar_init(&fullS[i], fc); mbar_init(&emptyS[i], NCW);
+      mbar_init(&fullX[i], fc); mbar_init(&emptyX[i], NCW);
+    }
+    if (TMA) {
+      tma_prefetch_map(&a.mapX);
+      tma_prefetch_map(&a.mapL);
+      tma_prefetch_map(&a.mapS);
+    }
+  }
+  __syncthreads();
+
+  if (warp == PRODUCER) {
+    int vL = 0, vS = 0, vX = 0;
+    for (int u = 0; u < units; ++u) {
+      const int tl = u / (nxc * nkc), rem = u % (nxc * nkc), xc = rem / nkc, kc = rem % nkc;
+      const int64_t row0 = (first + (int64_t)tl * stride) * TR;
+      if (newX(u)) {
+        const int sl = vX & 1, use = vX >> 1;
+        if (use > 0) mbar_wait(&emptyX[sl], (use - 1) & 1);
+        if (TMA) {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&fullX[sl], TILE_BYTES);
+            tma_load_2d(ringX + sl * TILE, &a.mapX, (int)row0, xc * 64, &fullX[sl]);
+          }
+        } else {
+          produce_tile<TR, LDT, false, 64>(ringX + sl * TILE, a.X, a.ldx, row0, a.m, xc * 64, a.q, lane);
+          cp_async_arrive(&fullX[sl]);
+        }
+        ++vX;
+      }
+      if (newL(u)) {
+        const int sl = vL & 1, use = vL >> 1;
+        if (use > 0) mbar_wait(&emptyL[sl], (use - 1) & 1);
+        if (TMA) {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&fullL[sl], TILE_BYTES);
+            tma_load_2d(ringL + sl * TILE, &a.mapL, (int)row0, kc * 64, &fullL[sl]);
+          }
+        } else {
+          produce_tile<TR, LDT, false, 64>(ringL + sl * TILE, a.L, a.ldl, row0, a.m, kc * 64, a.p, lane);
+          cp_async_arrive(&fullL[sl]);
+        }
+        ++vL;
+      }
+      if (newS(u)) {
+        const int sl = vS & 1, use = vS >> 1;
+        if (use > 0) mbar_wait(&emptyS[sl], (use - 1) & 1);
+        // S chunk (kc, xc): rows (k) kc*64.., columns xc*64.. of the p x q matrix S
+        if (TMA) {
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&fullS[sl], TILE_BYTES);
+            tma_load_2d(ringS + sl * TILE, &a.mapS, kc * 64, xc * 64, &fullS[sl]);
+          }
+        } else {
+          produce_tile<64, LDT, false, 64>(ringS + sl * TILE, a.S, a.lds, (int64_t)kc * 64, a.p, xc * 64, a.q, lane);
+          cp_async_arrive(&fullS[sl]);
+        }
+        ++vS;
+      }
+    }
+    return;
+  }
+
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wr = warp >> 2, wc = warp & 3;
+  double acc[4][2][2];
+  double g[10];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) g[i] = 0.0;
+  int vL = 0, vS = 0, vX = 0;
+  for (int u = 0; u < units; ++u) {
+    const int tl = u / (nxc * nkc), rem = u % (nxc * nkc), xc = rem / nkc, kc = rem % nkc;
+    const int64_t row0 = (first + (int64_t)tl * stride) * TR;
+    const bool gram_here = fuse_gram && xc == 0;
+    if (newX(u)) {
+      const int slX = vX & 1;
+      mbar_wait(&fullX[slX], (vX >> 1) & 1);
+      const double* sX = ringX + slX * TILE;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int r = wr * 32 + i * 8 + gid, c = wc * 16 + j * 8 + 2 * tig;
+          acc[i][j][0] = -sX[c * LDT + r];
+          acc[i][j][1] = -sX[(c + 1) * LDT + r];
+        }
+      if (!gram_here) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyX[slX]);
+      }
+      ++vX;
+    }
+    const int slL = (vL - (newL(u) ? 0 : 1)) & 1;
+    if (newL(u)) {
+      mbar_wait(&fullL[slL], (vL >> 1) & 1);
+      ++vL;
+    }
+    const int slS = (vS - (newS(u) ? 0 : 1)) & 1;
+    if (newS(u)) {
+      mbar_wait(&fullS[slS], (vS >> 1) & 1);
+      ++vS;
+    }
+    const double* sL = ringL + slL * TILE;
+    const double* sS = ringS + slS * TILE;
+    // k beyond p is zero-filled in both L and S: the full 64-wide chunk is exact
+#pragma unroll 4
+    for (int k0 = 0; k0 < 64; k0 += 4) {
+      double fa[4], fb[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = sL[(k0 + tig) * LDT + wr * 32 + i * 8 + gid];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) fb[j] = sS[(wc * 16 + j * 8 + gid) * LDT + k0 + tig];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+    // release L / S when the next unit stages a new version (or at the end)
+    if (u + 1 == units || newL(u + 1)) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyL[slL]);
+    }
+    if (u + 1 == units || newS(u + 1)) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyS[slS]);
+    }
+    if (kc == nkc - 1) {
+      // X <- -acc : straight to global from the fragments
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t r = row0 + wr * 32 + i * 8 + gid;
+        if (r < a.m) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int c = xc * 64 + wc * 16 + j * 8 + 2 * tig;
+            if (c < a.q) a.X[r + (int64_t)c * a.ldx] = -acc[i][j][0];
+            if (c + 1 < a.q) a.X[r + (int64_t)(c + 1) * a.ldx] = -acc[i][j][1];
+          }
+        }
+      }
+      if (gram_here) {
+        // fused Gram of the updated 64-column chunk: write it back into its X slot (each
+        // warp owns its region), then every warp accumulates its upper 8x8 blocks
+        const int sl = (vX - 1) & 1;
+        double* sX = ringX + sl * TILE;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int r = wr * 32 + i * 8 + gid, c = wc * 16 + j * 8 + 2 * tig;
+            const bool ok = row0 + r < a.m;  // rows past m stay exactly zero
+            sX[c * LDT + r] = ok ? -acc[i][j][0] : 0.0;
+            sX[(c + 1) * LDT + r] = ok ? -acc[i][j][1] : 0.0;
+          }
+        consumer_sync();
+        gram_tile_blocks<LDT>(sX, warp, gid, tig, g);
+        fence_proxy_async();  // generic writes above precede the next TMA fill of this slot
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyX[sl]);
+      }
+    }
+  }
+  if (fuse_gram) gram_blocks_store(a.gram_part + (int64_t)blockIdx.x * 4096, warp, gid, tig, g);
+}
+
+// =========================================================================================
+// k_trmm: X (m x B) <- X * Z in place, Z upper triangular (B x B): panel orthogonalisation
+// Q = A R^{-1} with the explicit inverse (Alg. 1 l.3 P:133; R-4).  Row tiles are streamed
+// through a 3-stage ring; warp w owns a row group and balanced column-block pairs
+// (cb, NB-1-cb) so the triangular work is even.  Z is in shared memory for B <= 64, read
+// through L1/L2 otherwise.  Optional fused epilogue (B == 64, gram_part != nullptr): Gram
+// of the new tile (the next CholeskyQR's Gram, Alg. 3 l.2) per CTA.
+// =========================================================================================
+template <int B>
+struct TrmmCfg {
+  static constexpr int NB = B / 8;
+  static constexpr int PAIRS = NB / 2;
+  static constexpr int PAIRS_PER_WARP = PAIRS >= NCW ? PAIRS / NCW : 1;
+  static constexpr int ROW_GROUPS = PAIRS >= NCW ? 1 : NCW / PAIRS;
+  static constexpr int TRR = (B <= 64) ? 64 : 32;
+  static constexpr int LD = TRR + 4;
+  static constexpr int RB = TRR / 8 / ROW_GROUPS;
+  static constexpr bool ZSMEM = (B <= 64);
+  static constexpr int LDZ = B + 4;
+  static constexpr int NS = 3;
+  static constexpr int BOXC = B < 64 ? B : 64;  // columns per TMA box
+  static constexpr int TILE_DBL = B * LD;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)NS * TILE_DBL + (ZSMEM ? (size_t)B * LDZ : 0)) +
+                                 2 * NS * sizeof(uint64_t) + 128;
+};
+
+struct TrmmArgs {
+  CUtensorMap mapX;  // X: rows m, cols B, box (LD rows, BOXC cols)
+  double* X;
+  int64_t ldx;
+  int64_t m;
+  const double* Z;
+  int ldz;
+  double* gram_part;
+  const int* status;
+};
+
+template <int B, bool TMA>
+__global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmArgs a) {
+  using C = TrmmCfg<B>;
+  extern __shared__ __align__(128) double smem_raw[];
+  if (failed(a.status)) return;
+  double* smem = aligned_smem(smem_raw);
+  double* ring = smem;
+  double* sZ = smem + C::NS * C::TILE_DBL;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sZ + (C::ZSMEM ? B * C::LDZ : 0));
+  uint64_t* empty = full + C::NS;
+  double* X = a.X;
+  const int64_t ldx = a.ldx, m = a.m;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntr = (m + C::TRR - 1) / C::TRR;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int nmine = (int)(first < ntr ? (ntr - 1 - first) / stride + 1 : 0);
+  const bool fuse_gram = (B == 64) && a.gram_part != nullptr;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::NS; ++i) {
+      mbar_init(&full[i], TMA ? 1 : 32);
+      mbar_init(&empty[i], NCW);
+    }
+    if (TMA) tma_prefetch_map(&a.mapX);
+  }
+  __syncthreads();
+
+  if (warp == PRODUCER) {
+    for (int it = 0; it < nmine; ++it) {
+      const int st = it % C::NS, use = it / C::NS;
+      if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
+      const int64_t row0 = (first + (int64_t)it * stride) * C::TRR;
+      if (TMA) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[st], (uint32_t)(C::TILE_DBL * 8));
+          for (int c0 = 0; c0 < B; c0 += 64)
+            tma_load_2d(ring + st * C::TILE_DBL + c0 * C::LD, &a.mapX, (int)row0, c0, &full[st]);
+        }
+      } else {
+        for (int c0 = 0; c0 < B; c0 += 64)
+          produce_tile<C::TRR, C::LD, false, C::BOXC>(ring + st * C::TILE_DBL + c0 * C::LD, X, ldx, row0, m, c0, B,
+                                                      lane);
+        cp_async_arrive(&full[st]);
+      }
+    }
+    return;
+  }
+
+  if (C::ZSMEM) {
+    for (int e = threadIdx.x; e < B * B; e += NCW * 32) {
+      const int k = e % B, col = e / B;
+      sZ[col * C::LDZ + k] = a.Z[k + (int64_t)col * a.ldz];
+    }
+    consumer_sync();
+  }
+  const int gid = lane >> 2, tig = lane & 3;
+  const int rg = warp % C::ROW_GROUPS, pw = warp / C::ROW_GROUPS;
+  constexpr int CBW = 2 * C::PAIRS_PER_WARP;
+  int cbs[CBW];
+#pragma unroll
+  for (int u = 0; u < C::PAIRS_PER_WARP; ++u) {
+    const int pr = pw * C::PAIRS_PER_WARP + u;
+    cbs[2 * u] = pr;
+    cbs[2 * u + 1] = C::NB - 1 - pr;
+  }
+  int maxcb = 0;
+#pragma unroll
+  for (int u = 0; u < CBW; ++u) maxcb = cbs[u] > maxcb ? cbs[u] : maxcb;
+  double g[10];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) g[i] = 0.0;
+
+  for (int it = 0; it < nmine; ++it) {
+    const int st = it % C::NS;
+    mbar_wait(&full[st], (it / C::NS) & 1);
+    double* sX = ring + st * C::TILE_DBL;
+    const int64_t row0 = (first + (int64_t)it * stride) * C::TRR;
+    double acc[C::RB][CBW][2];
+#pragma unroll
+    for (int i = 0; i < C::RB; ++i)
+#pragma unroll
+      for (int u = 0; u < CBW; ++u) acc[i][u][0] = acc[i][u][1] = 0.0;
+    const int kend = (maxcb + 1) * 8;
+    for (int k0 = 0; k0 < kend; k0 += 4) {
+      double fa[C::RB];
+#pragma unroll
+      for (int i = 0; i < C::RB; ++i) fa[i] = sX[(k0 + tig) * C::LD + (rg * C::RB + i) * 8 + gid];
+#pragma unroll
+      for (int u = 0; u < CBW; ++u) {
+        if (k0 < (cbs[u] + 1) * 8) {
+          const int col = cbs[u] * 8 + gid;
+          const double fb =
+              C::ZSMEM ? sZ[col * C::LDZ + k0 + tig] : __ldg(a.Z + (k0 + tig) + (int64_t)col * a.ldz);
+#pragma unroll
+          for (int i = 0; i < C::RB; ++i) dmma(acc[i][u][0], acc[i][u][1], fa[i], fb);
+        }
+      }
+    }
+    if (!fuse_gram) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int i = 0; i < C::RB; ++i) {
+      const int64_t r = row0 + (rg * C::RB + i) * 8 + gid;
+      if (r < m) {
+#pragma unroll
+        for (int u = 0; u < CBW; ++u) {
+          const int c = cbs[u] * 8 + 2 * tig;
+          X[r + (int64_t)c * ldx] = acc[i][u][0];
+          X[r + (int64_t)(c + 1) * ldx] = acc[i][u][1];
+        }
+      }
+    }
+    if (fuse_gram) {
+      consumer_sync();  // every warp has finished reading the old tile
+#pragma unroll
+      for (int i = 0; i < C::RB; ++i) {
+        const int r = (rg * C::RB + i) * 8 + gid;
+#pragma unroll
+        for (int u = 0; u < CBW; ++u) {
+          const int c = cbs[u] * 8 + 2 * tig;
+          sX[c * C::LD + r] = acc[i][u][0];
+          sX[(c + 1) * C::LD + r] = acc[i][u][1];
+        }
+      }
+      consumer_sync();
+      gram_tile_blocks<C::LD>(sX, warp, gid, tig, g);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  if (fuse_gram) gram_blocks_store(a.gram_part + (int64_t)blockIdx.x * 4096, warp, gid, tig, g);
+}
+
+}  // namespace tsqr

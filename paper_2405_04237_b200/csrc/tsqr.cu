@@ -5,6 +5,8 @@
 // kernels.cuh, every cross-GPU sum is one in-stream ncclAllReduce(ncclFloat64, ncclSum) of
 // a small replicated block (b x b Gram, b x N projection, (j-1)b x b re-orthogonalisation
 // block), and Cholesky / R assembly run redundantly on every rank.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -74,7 +76,7 @@ AtbShape atb_shape(int64_t m, int p, int q, bool gram) {
   s.ntp = (p + 63) / 64;
   s.ntq = (q + 63) / 64;
   s.tiles = gram ? s.ntq * (s.ntq + 1) / 2 : s.ntp * s.ntq;
-  const int64_t ntr = (m + ATB_TR - 1) / ATB_TR;
+  const int64_t ntr = (m + TR - 1) / TR;
   int S = s.tiles >= kSMs ? 1 : kSMs / s.tiles;
   const int64_t maxS = std::max<int64_t>(1, ntr / 4);  // >= 4 row tiles per split
   if (S > maxS) S = (int)maxS;
@@ -90,13 +92,50 @@ size_t atb_part_doubles(int64_t m, int p, int q, bool gram) {
   return (size_t)s.S * (size_t)p * (size_t)q;
 }
 
-bool v16_ok(const void* ptr, int64_t ld) {
-  return ((reinterpret_cast<uintptr_t>(ptr) & 15u) == 0) && (ld % 2 == 0);
-}
-
 int grid_1d(int64_t n, int nt = 256) {
   int64_t g = (n + nt - 1) / nt;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 4 * kSMs));
+}
+
+// ---- TMA tensor maps (cuTensorMapEncodeTiled fetched through the runtime: no -lcuda) ----
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+tsqr_status tma_encoder() {
+  if (g_encode) return TSQR_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || !fn) {
+    set_err("cuTensorMapEncodeTiled unavailable");
+    return TSQR_ERR_CUDA;
+  }
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return TSQR_OK;
+}
+
+// column-major FP64 matrix (rows x cols, leading dimension ld) as a 2-D tensor map with a
+// (box_rows x box_cols) box; out-of-bounds elements read as zero
+tsqr_status make_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                     int box_cols) {
+  TRY(tma_encoder());
+  cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(rows, 1), (cuuint64_t)std::max<int64_t>(cols, 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_err("cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld ld=%lld", (int)r, (long long)rows,
+            (long long)cols, (long long)ld);
+    return TSQR_ERR_CUDA;
+  }
+  return TSQR_OK;
+}
+
+// TMA needs a 16-byte aligned base, 16-byte multiple strides and at least one row
+bool tma_ok(const void* ptr, int64_t ld, int64_t rows) {
+  return rows > 0 && ((reinterpret_cast<uintptr_t>(ptr) & 15u) == 0) && (ld % 2 == 0);
 }
 
 // ---- optional per-kernel-class event timing ----
@@ -149,6 +188,13 @@ struct Timer {
 };
 
 // ---- kernel launchers (single GPU, enqueue only) ----
+constexpr int kGramParts = kSMs;  // CTAs of the fused-Gram kernels = partials to reduce
+
+template <typename K>
+cudaError_t set_smem(K kernel, size_t bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 struct Launcher {
   cudaStream_t st = nullptr;
   int64_t launches = 0;
@@ -158,88 +204,123 @@ struct Launcher {
   size_t tbegin() { return timer ? timer->begin(st) : (size_t)-1; }
   void tend(size_t e0, int cls, double flops, double bytes) { if (timer) timer->end(st, e0, cls, flops, bytes); }
 
+  tsqr_status reduce(const double* part, int S, int p, int q, int ldp, int64_t pstride, double* out, int ldo,
+                     bool gram) {
+    k_reduce<<<grid_1d((int64_t)p * q), 256, 0, st>>>(part, S, p, q, ldp, pstride, out, ldo, gram ? 1 : 0, status);
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    return TSQR_OK;
+  }
+
+  // OUT (p x q, ldo) = L^T R summed over all m rows (split-row partials + fixed-order reduce)
   tsqr_status atb(const double* L, int64_t ldl, const double* R, int64_t ldr, int64_t m, int p, int q, bool gram,
                   double* part, double* out, int ldo) {
     AtbShape sh = atb_shape(m, p, q, gram);
-    AtbArgs a{L, ldl, R, ldr, m, p, q, gram ? 1 : 0, sh.ntp, sh.ntq, sh.tps, part, status};
+    ProjArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.L = L; a.ldl = ldl; a.R = R; a.ldr = ldr; a.m = m; a.p = p; a.q = q; a.gram = gram ? 1 : 0;
+    a.ntp = sh.ntp; a.ntq = sh.ntq; a.tiles_per_split = sh.tps; a.part = part; a.status = status;
     dim3 grid(sh.tiles, sh.S);
+    const bool tma = tma_ok(L, ldl, m) && tma_ok(R, ldr, m);
+    if (tma) {
+      TRY(make_map(&a.mapL, L, m, p, ldl, LDT, 64));
+      TRY(make_map(&a.mapR, R, m, q, ldr, LDT, 64));
+    }
     const size_t t0 = tbegin();
-    const bool v16 = v16_ok(L, ldl) && v16_ok(R, ldr);
-    if (v16) {
-      CUDA_TRY(cudaFuncSetAttribute(k_atb<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ATB_SMEM));
-      k_atb<true><<<grid, NT, ATB_SMEM, st>>>(a);
+    if (tma) {
+      CUDA_TRY(set_smem(k_proj<true>, PROJ_SMEM));
+      k_proj<true><<<grid, NTHR, PROJ_SMEM, st>>>(a);
     } else {
-      CUDA_TRY(cudaFuncSetAttribute(k_atb<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ATB_SMEM));
-      k_atb<false><<<grid, NT, ATB_SMEM, st>>>(a);
+      CUDA_TRY(set_smem(k_proj<false>, PROJ_SMEM));
+      k_proj<false><<<grid, NTHR, PROJ_SMEM, st>>>(a);
     }
     CUDA_TRY(cudaGetLastError());
-    k_reduce<<<grid_1d((int64_t)p * q), 256, 0, st>>>(part, sh.S, p, q, out, ldo, gram ? 1 : 0, status);
-    CUDA_TRY(cudaGetLastError());
-    launches += 2;
+    launches += 1;
+    TRY(reduce(part, sh.S, p, q, p, (int64_t)p * q, out, ldo, gram));
     if (gram) tend(t0, TSQR_KCLASS_GRAM, (double)m * p * p, 8.0 * m * p);
     else tend(t0, TSQR_KCLASS_PROJ, 2.0 * m * p * q, 8.0 * m * (p + q));
     return TSQR_OK;
   }
 
+  // X <- X Z (in place); with gpart != nullptr (B == 64 only) also the per-CTA Gram of the
+  // result into gpart[kGramParts][64*64], reduced into Wout
   template <int B>
-  tsqr_status trmm_b(double* X, int64_t ldx, int64_t m, const double* Z, int ldz) {
+  tsqr_status trmm_b(double* X, int64_t ldx, int64_t m, const double* Z, int ldz, double* gpart, double* Wout) {
     using C = TrmmCfg<B>;
-    const int64_t ntr = (m + C::TR - 1) / C::TR;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntr, kSMs));
+    const int grid = kSMs;
+    TrmmArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.X = X; a.ldx = ldx; a.m = m; a.Z = Z; a.ldz = ldz; a.gram_part = gpart; a.status = status;
+    const bool tma = tma_ok(X, ldx, m);
+    if (tma) TRY(make_map(&a.mapX, X, m, B, ldx, C::LD, C::BOXC));
     const size_t t0 = tbegin();
-    if (v16_ok(X, ldx)) {
-      CUDA_TRY(cudaFuncSetAttribute(k_trmm<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      k_trmm<B, true><<<grid, NT, C::SMEM, st>>>(X, ldx, m, Z, ldz, status);
+    if (tma) {
+      CUDA_TRY(set_smem(k_trmm<B, true>, C::SMEM));
+      k_trmm<B, true><<<grid, NTHR, C::SMEM, st>>>(a);
     } else {
-      CUDA_TRY(cudaFuncSetAttribute(k_trmm<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      k_trmm<B, false><<<grid, NT, C::SMEM, st>>>(X, ldx, m, Z, ldz, status);
+      CUDA_TRY(set_smem(k_trmm<B, false>, C::SMEM));
+      k_trmm<B, false><<<grid, NTHR, C::SMEM, st>>>(a);
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
-    tend(t0, TSQR_KCLASS_TRMM, (double)m * B * B, 16.0 * m * B);
+    if (gpart) TRY(reduce(gpart, grid, B, B, 64, 4096, Wout, B, true));
+    tend(t0, TSQR_KCLASS_TRMM, (double)m * B * B + (gpart ? (double)m * B * B : 0.0), 16.0 * m * B);
     return TSQR_OK;
   }
 
-  tsqr_status trmm(double* X, int64_t ldx, int64_t m, int b, const double* Z, int ldz) {
+  tsqr_status trmm(double* X, int64_t ldx, int64_t m, int b, const double* Z, int ldz, double* gpart = nullptr,
+                   double* Wout = nullptr) {
+    if (b != 64) gpart = nullptr;
     switch (b) {
-      case 16: return trmm_b<16>(X, ldx, m, Z, ldz);
-      case 32: return trmm_b<32>(X, ldx, m, Z, ldz);
-      case 64: return trmm_b<64>(X, ldx, m, Z, ldz);
-      case 128: return trmm_b<128>(X, ldx, m, Z, ldz);
-      case 256: return trmm_b<256>(X, ldx, m, Z, ldz);
+      case 16: return trmm_b<16>(X, ldx, m, Z, ldz, nullptr, nullptr);
+      case 32: return trmm_b<32>(X, ldx, m, Z, ldz, nullptr, nullptr);
+      case 64: return trmm_b<64>(X, ldx, m, Z, ldz, gpart, Wout);
+      case 128: return trmm_b<128>(X, ldx, m, Z, ldz, nullptr, nullptr);
+      case 256: return trmm_b<256>(X, ldx, m, Z, ldz, nullptr, nullptr);
       default: set_err("trmm: unsupported b=%d", b); return TSQR_ERR_UNSUPPORTED;
     }
   }
 
+  // X (m x q) -= L (m x p) S (p x q); with gpart (q >= 64): the Gram of the updated first
+  // 64 columns, reduced into Wout (64 x 64)
   tsqr_status update(double* X, int64_t ldx, const double* L, int64_t ldl, const double* S, int64_t lds, int64_t m,
-                     int p, int q) {
-    UpdArgs a{X, ldx, L, ldl, S, lds, m, p, q, status};
-    const int64_t ntr = (m + UPD_TR - 1) / UPD_TR;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntr, kSMs));
+                     int p, int q, double* gpart = nullptr, double* Wout = nullptr) {
+    if (q < 64) gpart = nullptr;
+    UpdArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.X = X; a.ldx = ldx; a.L = L; a.ldl = ldl; a.S = S; a.lds = lds; a.m = m; a.p = p; a.q = q;
+    a.gram_part = gpart; a.status = status;
+    const int grid = kSMs;
+    const bool tma = tma_ok(X, ldx, m) && tma_ok(L, ldl, m) && tma_ok(S, lds, p);
+    if (tma) {
+      TRY(make_map(&a.mapX, X, m, q, ldx, LDT, 64));
+      TRY(make_map(&a.mapL, L, m, p, ldl, LDT, 64));
+      TRY(make_map(&a.mapS, S, p, q, lds, LDT, 64));
+    }
     const size_t t0 = tbegin();
-    if (v16_ok(L, ldl) && v16_ok(S, lds)) {
-      CUDA_TRY(cudaFuncSetAttribute(k_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UPD_SMEM));
-      k_update<true><<<grid, NT, UPD_SMEM, st>>>(a);
+    if (tma) {
+      CUDA_TRY(set_smem(k_update<true>, UPD_SMEM));
+      k_update<true><<<grid, NTHR, UPD_SMEM, st>>>(a);
     } else {
-      CUDA_TRY(cudaFuncSetAttribute(k_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UPD_SMEM));
-      k_update<false><<<grid, NT, UPD_SMEM, st>>>(a);
+      CUDA_TRY(set_smem(k_update<false>, UPD_SMEM));
+      k_update<false><<<grid, NTHR, UPD_SMEM, st>>>(a);
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
-    tend(t0, TSQR_KCLASS_UPDATE, 2.0 * m * p * q, 8.0 * m * (p + 2.0 * q));
+    if (gpart) TRY(reduce(gpart, grid, 64, 64, 64, 4096, Wout, 64, true));
+    tend(t0, TSQR_KCLASS_UPDATE, 2.0 * m * p * q + (gpart ? 64.0 * 64.0 * m : 0.0), 8.0 * m * (p + 2.0 * q));
     return TSQR_OK;
   }
 
   tsqr_status chol_inv(const double* W, int ldw, int b, double* U, int ldu, double* Z, int ldz, int* status_rw,
                        int pass, int panel, int stage, double* work) {
-    const bool sm = b <= 128;
-    const size_t smem = sm ? sizeof(double) * (size_t)b * b : 0;
-    if (sm) CUDA_TRY(cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t smem = sizeof(double) * (b <= 64 ? 2 * (size_t)b * b : (b <= 128 ? (size_t)b * b : 0));
+    CUDA_TRY(set_smem(k_chol_inv, smem > 0 ? smem : 1));
     const size_t t0 = tbegin();
-    k_chol_inv<<<1, CHOL_NT, smem, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage, work, sm ? 1 : 0);
+    k_chol_inv<<<1, CHOL_NT, smem, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage, work);
     CUDA_TRY(cudaGetLastError());
     launches += 1;
-    tend(t0, TSQR_KCLASS_CHOL, (double)b * b * b / 3.0 + (double)b * b * b / 3.0, 16.0 * b * b);
+    tend(t0, TSQR_KCLASS_CHOL, 2.0 * b * b * b / 3.0, 16.0 * b * b);
     return TSQR_OK;
   }
 
@@ -294,6 +375,8 @@ struct tsqr_plan_s {
   double* R1 = nullptr;      // n x n (CQR2GS pass 1 / CQR2 temporaries)
   double* R2 = nullptr;      // n x n
   double* cwork = nullptr;   // b x b Cholesky scratch for b > 128
+  double* gpart = nullptr;   // [kGramParts][64*64] fused-Gram partials (b == 64)
+  bool fuse = false;         // Gram fused into the update / TRMM epilogues (b == 64)
   Launcher L;
   Timer timer;
   int64_t allreduces = 0;
@@ -339,9 +422,10 @@ size_t carve(Carve& c, tsqr_plan_s* p, int64_t m, int n, int b, tsqr_algo algo) 
   double* R1 = c.take<double>((size_t)n * n);
   double* R2 = c.take<double>((size_t)n * n);
   double* cw = c.take<double>((size_t)b * b);
+  double* gp = c.take<double>(b == 64 ? (size_t)kGramParts * 4096 : 1);
   if (p) {
     p->status = status; p->part = part; p->W = W; p->Y = Y; p->U1 = U1; p->U2 = U2; p->Z = Z;
-    p->R1 = R1; p->R2 = R2; p->cwork = cw;
+    p->R1 = R1; p->R2 = R2; p->cwork = cw; p->gpart = gp;
   }
   return align_up(c.off);
 }
@@ -368,17 +452,28 @@ tsqr_status allreduce(tsqr_plan_s* P, double* buf, size_t count) {
   return TSQR_OK;
 }
 
-// W <- allreduce(X^T X), X = m x w slab
+// W <- allreduce(X^T X), X = m x w slab (standalone split-row Gram)
 tsqr_status gram(tsqr_plan_s* P, const double* X, int64_t ldx, int w) {
   TRY(P->L.atb(X, ldx, X, ldx, P->m, w, w, true, P->part, P->W, w));
   return allreduce(P, P->W, (size_t)w * w);
 }
 
+// Cholesky + inverse of the (already allreduced) Gram W, then X <- X U^{-1}.  With
+// gram_next the TRMM epilogue also forms the Gram of the new X and allreduces it into W
+// (the next CholeskyQR's Gram, fused: saves re-reading the panel).
+tsqr_status chol_trmm(tsqr_plan_s* P, double* X, int64_t ldx, int w, double* Uout, int ldu, int pass, int panel,
+                      int stage, bool gram_next) {
+  TRY(P->L.chol_inv(P->W, w, w, Uout, ldu, P->Z, w, P->status, pass, panel, stage, P->cwork));
+  const bool f = gram_next && P->fuse && w == 64;
+  TRY(P->L.trmm(X, ldx, P->m, w, P->Z, w, f ? P->gpart : nullptr, f ? P->W : nullptr));
+  if (f) TRY(allreduce(P, P->W, (size_t)w * w));
+  return TSQR_OK;
+}
+
 // CholeskyQR of the m x w slab X in place (Alg. 2): U -> Uout (ldu), X <- X U^{-1}
 tsqr_status cqr(tsqr_plan_s* P, double* X, int64_t ldx, int w, double* Uout, int ldu, int pass, int panel, int stage) {
   TRY(gram(P, X, ldx, w));
-  TRY(P->L.chol_inv(P->W, w, w, Uout, ldu, P->Z, w, P->status, pass, panel, stage, P->cwork));
-  return P->L.trmm(X, ldx, P->m, w, P->Z, w);
+  return chol_trmm(P, X, ldx, w, Uout, ldu, pass, panel, stage, false);
 }
 
 // OUT (p x q, ld p) <- allreduce(L^T Rm)
@@ -387,18 +482,40 @@ tsqr_status proj(tsqr_plan_s* P, const double* Lm, int64_t ldl, int p, const dou
   return allreduce(P, out, (size_t)p * q);
 }
 
-// one CQRGS pass (Alg. 7) writing its R into Rp (ld n)
+// X (m x q) -= L S; with gram_next (fused path) also W <- allreduce(Gram of X's first 64 columns)
+tsqr_status update(tsqr_plan_s* P, double* X, int64_t ldx, const double* Lm, int64_t ldl, const double* S, int lds,
+                   int p, int q, bool gram_next) {
+  const bool f = gram_next && P->fuse && q >= 64;
+  TRY(P->L.update(X, ldx, Lm, ldl, S, lds, P->m, p, q, f ? P->gpart : nullptr, f ? P->W : nullptr));
+  if (f) TRY(allreduce(P, P->W, (size_t)64 * 64));
+  return TSQR_OK;
+}
+
+// CQR2 of the first b columns (Alg. 3; Alg. 8 l.1): U1, U2 -> R_11 = U2 U1
+tsqr_status cqr2_block(tsqr_plan_s* P, double* A, int64_t lda, int w, double* R, int ldr) {
+  TRY(gram(P, A, lda, w));
+  TRY(chol_trmm(P, A, lda, w, P->U1, w, 1, 1, 1, true));
+  if (!(P->fuse && w == 64)) TRY(gram(P, A, lda, w));
+  TRY(chol_trmm(P, A, lda, w, P->U2, w, 1, 1, 2, false));
+  return P->L.trimul(P->U2, w, P->U1, w, R, ldr, w);
+}
+
+// one CQRGS pass (Alg. 7) writing its R into Rp (ld ldr)
 tsqr_status cqrgs_pass(tsqr_plan_s* P, double* A, int64_t lda, double* Rp, int ldr, int pass) {
   const int n = P->n, b = P->b, k = P->k;
+  bool have_gram = false;  // W already holds the Gram of panel j (fused into the previous update)
   for (int j = 0; j < k; ++j) {
     double* Aj = A + (int64_t)j * b * lda;
-    // R_jj = U (chol writes straight into R's diagonal block)
-    TRY(cqr(P, Aj, lda, b, Rp + (int64_t)j * b + (int64_t)j * b * ldr, ldr, pass, j + 1, 1));
+    if (!have_gram) TRY(gram(P, Aj, lda, b));                                  // l.2-3
+    // l.4-6: R_jj = U (the Cholesky writes straight into R's diagonal block)
+    TRY(chol_trmm(P, Aj, lda, b, Rp + (int64_t)j * b + (int64_t)j * b * ldr, ldr, pass, j + 1, 1, false));
     const int nt = n - (j + 1) * b;
+    have_gram = false;
     if (nt > 0) {
       double* At = A + (int64_t)(j + 1) * b * lda;
       TRY(proj(P, Aj, lda, b, At, lda, nt, P->Y));                            // l.7-8
-      TRY(P->L.update(At, lda, Aj, lda, P->Y, b, P->m, b, nt));               // l.9
+      TRY(update(P, At, lda, Aj, lda, P->Y, b, b, nt, true));                 // l.9 (+ Gram of A_{j+1})
+      have_gram = P->fuse;
       TRY(P->L.copy2d(P->Y, b, Rp + (int64_t)j * b + (int64_t)(j + 1) * b * ldr, ldr, b, nt));  // l.10
     }
   }
@@ -407,26 +524,25 @@ tsqr_status cqrgs_pass(tsqr_plan_s* P, double* A, int64_t lda, double* Rp, int l
 
 tsqr_status run_mcqr2gs(tsqr_plan_s* P, double* A, int64_t lda, double* R, int ldr) {
   const int n = P->n, b = P->b, k = P->k;
-  // l.1: CQR2 of panel 1
-  TRY(cqr(P, A, lda, b, P->U1, b, 1, 1, 1));
-  TRY(cqr(P, A, lda, b, P->U2, b, 1, 1, 2));
-  TRY(P->L.trimul(P->U2, b, P->U1, b, R, ldr, b));
+  TRY(cqr2_block(P, A, lda, b, R, ldr));                                      // l.1
   for (int j = 1; j < k; ++j) {
     double* Ap = A + (int64_t)(j - 1) * b * lda;  // Q_{j-1}
     double* Aj = A + (int64_t)j * b * lda;
     const int Nj = n - j * b;
-    // l.3-5: Y = Q_{j-1}^T A_{:,j:k}; A_{:,j:k} -= Q_{j-1} Y; R_{j-1,j:k} = Y
+    // l.3-5: Y = Q_{j-1}^T A_{:,j:k}; A_{:,j:k} -= Q_{j-1} Y (+ Gram of A_j); R_{j-1,j:k} = Y
     TRY(proj(P, Ap, lda, b, Aj, lda, Nj, P->Y));
-    TRY(P->L.update(Aj, lda, Ap, lda, P->Y, b, P->m, b, Nj));
+    TRY(update(P, Aj, lda, Ap, lda, P->Y, b, b, Nj, true));
     TRY(P->L.copy2d(P->Y, b, R + (int64_t)(j - 1) * b + (int64_t)j * b * ldr, ldr, b, Nj));
     // l.6: first CQR, panel -> V1, keep U1
-    TRY(cqr(P, Aj, lda, b, P->U1, b, 1, j + 1, 1));
-    // l.7: C = Q_{1:j-1}^T V1 ((j-1)b x b); V1 -= Q_{1:j-1} C
+    if (!P->fuse) TRY(gram(P, Aj, lda, b));
+    TRY(chol_trmm(P, Aj, lda, b, P->U1, b, 1, j + 1, 1, false));
+    // l.7: C = Q_{1:j-1}^T V1 ((j-1)b x b); V1 -= Q_{1:j-1} C (+ Gram of V1')
     const int jb = j * b;
     TRY(proj(P, A, lda, jb, Aj, lda, b, P->Y));
-    TRY(P->L.update(Aj, lda, A, lda, P->Y, jb, P->m, jb, b));
+    TRY(update(P, Aj, lda, A, lda, P->Y, jb, jb, b, true));
     // l.8: second CQR -> Q_j, U2
-    TRY(cqr(P, Aj, lda, b, P->U2, b, 1, j + 1, 2));
+    if (!P->fuse) TRY(gram(P, Aj, lda, b));
+    TRY(chol_trmm(P, Aj, lda, b, P->U2, b, 1, j + 1, 2, false));
     // R_jj = U2 U1; R_{1:j-1,j} += C U1  (R-8)
     TRY(P->L.trimul(P->U2, b, P->U1, b, R + (int64_t)jb + (int64_t)jb * ldr, ldr, b));
     TRY(P->L.gemm_acc_tri(P->Y, jb, P->U1, b, R + (int64_t)jb * ldr, ldr, jb, b));
@@ -507,6 +623,7 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
   tsqr_plan_s* p = new (std::nothrow) tsqr_plan_s();
   if (!p) return TSQR_ERR_INVALID_ARG;
   p->m = m_local; p->n = n; p->b = panel_b; p->k = n / panel_b; p->algo = algo;
+  p->fuse = (panel_b == 64);
   p->comm = comm; p->nranks = nranks; p->rank = rank; p->stream = stream;
   Carve c;
   c.base = reinterpret_cast<char*>(workspace);
@@ -539,14 +656,16 @@ tsqr_status tsqr_factor(tsqr_plan_t P, double* A, int64_t lda, double* R, int32_
       s = cqr(P, A, lda, n, R, ldr, 1, 1, 1);
       break;
     case TSQR_CQR2:
-      s = cqr(P, A, lda, n, P->U1, n, 1, 1, 1);
-      if (s == TSQR_OK) s = cqr(P, A, lda, n, P->U2, n, 1, 1, 2);
-      if (s == TSQR_OK) s = P->L.trimul(P->U2, n, P->U1, n, R, ldr, n);
+      s = cqr2_block(P, A, lda, n, R, ldr);
       break;
     case TSQR_CQRGS:
       s = cqrgs_pass(P, A, lda, R, ldr, 1);
       break;
     case TSQR_CQR2GS:
+      if (P->k == 1) {  // b == n: CQR2GS falls back to CholeskyQR2
+        s = cqr2_block(P, A, lda, n, R, ldr);
+        break;
+      }
       k_zero2d<<<grid_1d((int64_t)n * n), 256, 0, P->stream>>>(P->R1, n, n, n);
       k_zero2d<<<grid_1d((int64_t)n * n), 256, 0, P->stream>>>(P->R2, n, n, n);
       P->L.launches += 2;
