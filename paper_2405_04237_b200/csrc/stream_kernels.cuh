@@ -22,9 +22,10 @@ constexpr int LDT = TR + 4;           // padded leading dimension (== 4 mod 16) 
 constexpr int TILE = 64 * LDT;        // doubles in one 64-column tile
 constexpr uint32_t TILE_BYTES = TILE * 8;
 
-// smem base rounded up to 128 bytes (TMA destinations); callers request +128 bytes
+// smem base rounded up to 128 bytes (TMA destinations); callers request +128 bytes.  Pointer
+// arithmetic on the __shared__ array keeps the address space, so accesses stay LDS/STS.
 __device__ __forceinline__ double* aligned_smem(double* p) {
-  return reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+  return p + (((128u - (smem_u32(p) & 127u)) & 127u) >> 3);
 }
 
 // =========================================================================================
