@@ -241,6 +241,130 @@ struct UpdArgs {
   const int* status;
 };
 
+// ---- k_update consumer helpers ----
+struct UpdCtx {
+  const UpdArgs& a;
+  double *ringL, *ringS, *ringX;
+  uint64_t *fullL, *emptyL, *fullS, *emptyS, *fullX, *emptyX;
+  int warp, lane, gid, tig, wr, wc, nxc, nkc;
+  int64_t first, stride;
+  bool fuse_gram;
+};
+struct UpdState {
+  int u = 0, vL = 0, vS = 0, vX = 0;  // unit counter and operand versions (same walk as the producer)
+  bool pend = false;
+  int64_t prow0 = 0;
+  int pxc = 0;
+};
+
+__device__ __forceinline__ bool upd_newL(const UpdCtx& c, int u) { return c.nkc > 1 || (u % c.nxc) == 0; }
+__device__ __forceinline__ bool upd_newS(const UpdCtx& c, int u) { return (c.nkc > 1 || c.nxc > 1) || u == 0; }
+
+// X <- -acc for chunk (row0, xc), straight from the fragments
+__device__ __forceinline__ void upd_store(const UpdCtx& c, int64_t row0, int xc, const double (&acc)[4][2][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = row0 + c.wr * 32 + i * 8 + c.gid;
+    if (r < c.a.m) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int col = xc * 64 + c.wc * 16 + j * 8 + 2 * c.tig;
+        if (col < c.a.q) c.a.X[r + (int64_t)col * c.a.ldx] = -acc[i][j][0];
+        if (col + 1 < c.a.q) c.a.X[r + (int64_t)(col + 1) * c.a.ldx] = -acc[i][j][1];
+      }
+    }
+  }
+}
+
+// one chunk (tile, xc) = nkc units into `acc`; `other` holds the pending result of the
+// previous chunk (stored after this chunk's first k-chunk)
+__device__ __forceinline__ void upd_chunk(const UpdCtx& c, UpdState& s, int ch, double (&acc)[4][2][2],
+                                          double (&other)[4][2][2], double (&g)[10]) {
+  const int tl = ch / c.nxc, xc = ch % c.nxc;
+  const int64_t row0 = (c.first + (int64_t)tl * c.stride) * TR;
+  const bool gram_here = c.fuse_gram && xc == 0;
+  // accumulators <- -X from the chunk's X slot
+  const int slX = s.vX & 1;
+  mbar_wait(&c.fullX[slX], (s.vX >> 1) & 1);
+  double* sX = c.ringX + slX * TILE;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int r = c.wr * 32 + i * 8 + c.gid, col = c.wc * 16 + j * 8 + 2 * c.tig;
+      acc[i][j][0] = -sX[col * LDT + r];
+      acc[i][j][1] = -sX[(col + 1) * LDT + r];
+    }
+  if (!gram_here) {
+    __syncwarp();
+    if (c.lane == 0) mbar_arrive(&c.emptyX[slX]);
+  }
+  ++s.vX;
+  for (int kc = 0; kc < c.nkc; ++kc, ++s.u) {
+    const int u = s.u;
+    const bool nl = upd_newL(c, u), ns = upd_newS(c, u);
+    const int slL = (s.vL - (nl ? 0 : 1)) & 1;
+    if (nl) {
+      mbar_wait(&c.fullL[slL], (s.vL >> 1) & 1);
+      ++s.vL;
+    }
+    const int slS = (s.vS - (ns ? 0 : 1)) & 1;
+    if (ns) {
+      mbar_wait(&c.fullS[slS], (s.vS >> 1) & 1);
+      ++s.vS;
+    }
+    const double* sL = c.ringL + slL * TILE;
+    const double* sS = c.ringS + slS * TILE;
+    // k beyond p is zero-filled in both L and S: the full 64-wide chunk is exact
+#pragma unroll 4
+    for (int k0 = 0; k0 < 64; k0 += 4) {
+      double fa[4], fb[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = sL[(k0 + c.tig) * LDT + c.wr * 32 + i * 8 + c.gid];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) fb[j] = sS[(c.wc * 16 + j * 8 + c.gid) * LDT + k0 + c.tig];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+    // release L / S when the next unit stages a new version (no release is needed after the
+    // CTA's last unit: the producer has nothing left to stage)
+    __syncwarp();
+    if (c.lane == 0) {
+      if (upd_newL(c, u + 1)) mbar_arrive(&c.emptyL[slL]);
+      if (upd_newS(c, u + 1)) mbar_arrive(&c.emptyS[slS]);
+    }
+    if (kc == 0 && s.pend) {  // the previous chunk's result: its DMMAs have long completed
+      upd_store(c, s.prow0, s.pxc, other);
+      s.pend = false;
+    }
+  }
+  if (gram_here) {
+    upd_store(c, row0, xc, acc);
+    // fused Gram of the updated 64-column chunk: write it back into its X slot (each warp
+    // owns its region), then every warp accumulates its upper 8x8 blocks
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = c.wr * 32 + i * 8 + c.gid, col = c.wc * 16 + j * 8 + 2 * c.tig;
+        const bool ok = row0 + r < c.a.m;  // rows past m stay exactly zero
+        sX[col * LDT + r] = ok ? -acc[i][j][0] : 0.0;
+        sX[(col + 1) * LDT + r] = ok ? -acc[i][j][1] : 0.0;
+      }
+    consumer_sync();
+    gram_tile_blocks<LDT>(sX, c.warp, c.gid, c.tig, g);
+    fence_proxy_async();  // generic writes above precede the next TMA fill of this slot
+    __syncwarp();
+    if (c.lane == 0) mbar_arrive(&c.emptyX[slX]);
+  } else {
+    s.pend = true;
+    s.prow0 = row0;
+    s.pxc = xc;
+  }
+}
+
 template <bool TMA>
 __global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdArgs a) {
   extern __shared__ __align__(128) double smem_raw[];
@@ -332,106 +456,26 @@ __global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdA
     return;
   }
 
-  const int gid = lane >> 2, tig = lane & 3;
-  const int wr = warp >> 2, wc = warp & 3;
-  double acc[4][2][2];
+  // Consumers walk the chunks (tile, xc) with two accumulator sets: the result of chunk c
+  // stays "pending" and is stored only after chunk c+1's first k-chunk has been issued, so
+  // the accumulator drain never stalls the DMMA pipe (gram chunks are finished in place).
+  UpdCtx c{a, ringL, ringS, ringX, fullL, emptyL, fullS, emptyS, fullX, emptyX, warp, lane, lane >> 2, lane & 3,
+           warp >> 2, warp & 3, nxc, nkc, first, stride, fuse_gram};
+  double accA[4][2][2], accB[4][2][2];
   double g[10];
 #pragma unroll
   for (int i = 0; i < 10; ++i) g[i] = 0.0;
-  int vL = 0, vS = 0, vX = 0;
-  for (int u = 0; u < units; ++u) {
-    const int tl = u / (nxc * nkc), rem = u % (nxc * nkc), xc = rem / nkc, kc = rem % nkc;
-    const int64_t row0 = (first + (int64_t)tl * stride) * TR;
-    const bool gram_here = fuse_gram && xc == 0;
-    if (newX(u)) {
-      const int slX = vX & 1;
-      mbar_wait(&fullX[slX], (vX >> 1) & 1);
-      const double* sX = ringX + slX * TILE;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int r = wr * 32 + i * 8 + gid, c = wc * 16 + j * 8 + 2 * tig;
-          acc[i][j][0] = -sX[c * LDT + r];
-          acc[i][j][1] = -sX[(c + 1) * LDT + r];
-        }
-      if (!gram_here) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&emptyX[slX]);
-      }
-      ++vX;
-    }
-    const int slL = (vL - (newL(u) ? 0 : 1)) & 1;
-    if (newL(u)) {
-      mbar_wait(&fullL[slL], (vL >> 1) & 1);
-      ++vL;
-    }
-    const int slS = (vS - (newS(u) ? 0 : 1)) & 1;
-    if (newS(u)) {
-      mbar_wait(&fullS[slS], (vS >> 1) & 1);
-      ++vS;
-    }
-    const double* sL = ringL + slL * TILE;
-    const double* sS = ringS + slS * TILE;
-    // k beyond p is zero-filled in both L and S: the full 64-wide chunk is exact
-#pragma unroll 4
-    for (int k0 = 0; k0 < 64; k0 += 4) {
-      double fa[4], fb[2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) fa[i] = sL[(k0 + tig) * LDT + wr * 32 + i * 8 + gid];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) fb[j] = sS[(wc * 16 + j * 8 + gid) * LDT + k0 + tig];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
-    }
-    // release L / S when the next unit stages a new version (or at the end)
-    if (u + 1 == units || newL(u + 1)) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&emptyL[slL]);
-    }
-    if (u + 1 == units || newS(u + 1)) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&emptyS[slS]);
-    }
-    if (kc == nkc - 1) {
-      // X <- -acc : straight to global from the fragments
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t r = row0 + wr * 32 + i * 8 + gid;
-        if (r < a.m) {
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int c = xc * 64 + wc * 16 + j * 8 + 2 * tig;
-            if (c < a.q) a.X[r + (int64_t)c * a.ldx] = -acc[i][j][0];
-            if (c + 1 < a.q) a.X[r + (int64_t)(c + 1) * a.ldx] = -acc[i][j][1];
-          }
-        }
-      }
-      if (gram_here) {
-        // fused Gram of the updated 64-column chunk: write it back into its X slot (each
-        // warp owns its region), then every warp accumulates its upper 8x8 blocks
-        const int sl = (vX - 1) & 1;
-        double* sX = ringX + sl * TILE;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int r = wr * 32 + i * 8 + gid, c = wc * 16 + j * 8 + 2 * tig;
-            const bool ok = row0 + r < a.m;  // rows past m stay exactly zero
-            sX[c * LDT + r] = ok ? -acc[i][j][0] : 0.0;
-            sX[(c + 1) * LDT + r] = ok ? -acc[i][j][1] : 0.0;
-          }
-        consumer_sync();
-        gram_tile_blocks<LDT>(sX, warp, gid, tig, g);
-        fence_proxy_async();  // generic writes above precede the next TMA fill of this slot
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&emptyX[sl]);
-      }
-    }
+  UpdState st;
+  const int nch = nmine * nxc;
+  for (int ch = 0; ch < nch; ch += 2) {
+    upd_chunk(c, st, ch, accA, accB, g);
+    if (ch + 1 < nch) upd_chunk(c, st, ch + 1, accB, accA, g);
   }
-  if (fuse_gram) gram_blocks_store(a.gram_part + (int64_t)blockIdx.x * 4096, warp, gid, tig, g);
+  if (st.pend) {  // the last chunk (index nch-1) used accA when nch-1 is even
+    if (((nch - 1) & 1) == 0) upd_store(c, st.prow0, st.pxc, accA);
+    else upd_store(c, st.prow0, st.pxc, accB);
+  }
+  if (fuse_gram) gram_blocks_store(a.gram_part + (int64_t)blockIdx.x * 4096, warp, c.gid, c.tig, g);
 }
 
 // =========================================================================================
