@@ -22,10 +22,11 @@ constexpr int LDT = TR + 4;           // padded leading dimension (== 4 mod 16) 
 constexpr int TILE = 64 * LDT;        // doubles in one 64-column tile
 constexpr uint32_t TILE_BYTES = TILE * 8;
 
-// smem base rounded up to 128 bytes (TMA destinations); callers request +128 bytes.  Pointer
-// arithmetic on the __shared__ array keeps the address space, so accesses stay LDS/STS.
-__device__ __forceinline__ double* aligned_smem(double* p) {
-  return p + (((128u - (smem_u32(p) & 127u)) & 127u) >> 3);
+// smem base rounded up to `al` bytes (TMA destinations; 1024 for 128-byte swizzled boxes);
+// callers request +al bytes.  Pointer arithmetic on the __shared__ array keeps the address
+// space, so accesses stay LDS/STS.
+__device__ __forceinline__ double* aligned_smem(double* p, uint32_t al = 128) {
+  return p + (((al - (smem_u32(p) & (al - 1))) & (al - 1)) >> 3);
 }
 
 // =========================================================================================
@@ -223,10 +224,19 @@ __global__ void __launch_bounds__(NTHR, 1) k_proj(const __grid_constant__ ProjAr
 // columns (the next panel to be factored) accumulated per CTA into gram_part[blockIdx.x]
 // (64x64, upper blocks) -- the panel is not re-read for its CholeskyQR.
 // =========================================================================================
-constexpr size_t UPD_SMEM = sizeof(double) * (size_t)6 * TILE + 12 * sizeof(uint64_t) + 128;
+constexpr size_t UPD_SMEM = sizeof(double) * (size_t)6 * TILE + 12 * sizeof(uint64_t) + 1024;
+// TMA path: X slots hold a dense 64x64 tile in four 16-row boxes with the 128-byte swizzle
+constexpr int XSLOT = 64 * 64;
+
+// double index of element (column c, row r) of a swizzled X slot: box r/16 is [64 cols][16 rows],
+// the 16-byte chunk (r%16)/2 of column c is XORed with c%8 (CU_TENSOR_MAP_SWIZZLE_128B)
+__device__ __forceinline__ int xs_idx(int c, int r) {
+  return (r >> 4) * 1024 + c * 16 + (((((r & 15) >> 1) ^ (c & 7))) << 1) + (r & 1);
+}
 
 struct UpdArgs {
-  CUtensorMap mapX;  // X: rows m, cols q
+  CUtensorMap mapX;   // X: rows m, cols q, box (16 rows, 64 cols), 128-byte swizzle (loads)
+  CUtensorMap mapXs;  // X: rows m, cols q, box (16 rows, 16 cols), 128-byte swizzle (stores)
   CUtensorMap mapL;  // L: rows m, cols p
   CUtensorMap mapS;  // S: rows p, cols q
   double* X;
@@ -365,14 +375,110 @@ __device__ __forceinline__ void upd_chunk(const UpdCtx& c, UpdState& s, int ch, 
   }
 }
 
+// TMA-path chunk: -X from the swizzled slot, nkc k-chunks, then -acc written back into the
+// slot and stored by two per-warp TMA boxes (16 rows x 16 columns); the optional fused Gram
+// reads the updated chunk from the same slot.
+__device__ __forceinline__ void upd_chunk_tma(const UpdCtx& c, UpdState& s, int ch, double (&acc)[4][2][2],
+                                              double (&g)[10]) {
+  const int tl = ch / c.nxc, xc = ch % c.nxc;
+  const int64_t row0 = (c.first + (int64_t)tl * c.stride) * TR;
+  const bool gram_here = c.fuse_gram && xc == 0;
+  const int slX = s.vX & 1;
+  mbar_wait(&c.fullX[slX], (s.vX >> 1) & 1);
+  double* sX = c.ringX + slX * XSLOT;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int r = c.wr * 32 + i * 8 + c.gid, col = c.wc * 16 + j * 8 + 2 * c.tig;
+      acc[i][j][0] = -sX[xs_idx(col, r)];
+      acc[i][j][1] = -sX[xs_idx(col + 1, r)];
+    }
+  ++s.vX;
+  for (int kc = 0; kc < c.nkc; ++kc, ++s.u) {
+    const int u = s.u;
+    const bool nl = upd_newL(c, u), ns = upd_newS(c, u);
+    const int slL = (s.vL - (nl ? 0 : 1)) & 1;
+    if (nl) {
+      mbar_wait(&c.fullL[slL], (s.vL >> 1) & 1);
+      ++s.vL;
+    }
+    const int slS = (s.vS - (ns ? 0 : 1)) & 1;
+    if (ns) {
+      mbar_wait(&c.fullS[slS], (s.vS >> 1) & 1);
+      ++s.vS;
+    }
+    const double* sL = c.ringL + slL * TILE;
+    const double* sS = c.ringS + slS * TILE;
+#pragma unroll 4
+    for (int k0 = 0; k0 < 64; k0 += 4) {
+      double fa[4], fb[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = sL[(k0 + c.tig) * LDT + c.wr * 32 + i * 8 + c.gid];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) fb[j] = sS[(c.wc * 16 + j * 8 + c.gid) * LDT + k0 + c.tig];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+    __syncwarp();
+    if (c.lane == 0) {
+      if (upd_newL(c, u + 1)) mbar_arrive(&c.emptyL[slL]);
+      if (upd_newS(c, u + 1)) mbar_arrive(&c.emptyS[slS]);
+    }
+  }
+  // X <- -acc through the slot and two TMA stores per warp
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int r = c.wr * 32 + i * 8 + c.gid, col = c.wc * 16 + j * 8 + 2 * c.tig;
+      sX[xs_idx(col, r)] = -acc[i][j][0];
+      sX[xs_idx(col + 1, r)] = -acc[i][j][1];
+    }
+  fence_proxy_async();
+  __syncwarp();
+  if (c.lane == 0) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int box = 2 * c.wr + t;
+      tma_store_2d(&c.a.mapXs, (int)(row0 + 16 * box), xc * 64 + c.wc * 16, sX + box * 1024 + c.wc * 16 * 16);
+    }
+    bulk_commit();
+  }
+  if (gram_here) {
+    consumer_sync();  // every warp's part of the updated chunk is in the slot
+    int ao[5], bo[5];
+#pragma unroll
+    for (int v = 0; v < 5; ++v) {
+      int bi = 0, bj = 0;
+      if (c.warp + 8 * v < 36) upper_block(c.warp + 8 * v, bi, bj);
+      ao[v] = bi * 8 + c.gid;
+      bo[v] = bj * 8 + c.gid;
+    }
+    const bool has5 = c.warp + 32 < 36;
+#pragma unroll 2
+    for (int k0 = 0; k0 < 64; k0 += 4) {
+      const int r = k0 + c.tig;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
+      if (has5) dmma(g[8], g[9], sX[xs_idx(ao[4], r)], sX[xs_idx(bo[4], r)]);
+    }
+  }
+  if (c.lane == 0) bulk_wait_read0();  // the TMA stores have read the slot
+  __syncwarp();
+  if (c.lane == 0) mbar_arrive(&c.emptyX[slX]);
+}
+
 template <bool TMA>
 __global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdArgs a) {
   extern __shared__ __align__(128) double smem_raw[];
   if (failed(a.status)) return;
-  double* smem = aligned_smem(smem_raw);
+  double* smem = aligned_smem(smem_raw, 1024);
   double* ringL = smem;             // 2 slots
   double* ringS = smem + 2 * TILE;  // 2 slots
-  double* ringX = smem + 4 * TILE;  // 2 slots
+  double* ringX = smem + 4 * TILE;  // 2 slots (TMA path: 2 swizzled XSLOTs; 4*TILE*8 % 1024 == 0)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * TILE);
   uint64_t *fullL = bars, *emptyL = bars + 2, *fullS = bars + 4, *emptyS = bars + 6, *fullX = bars + 8,
            *emptyX = bars + 10;
@@ -398,6 +504,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdA
     }
     if (TMA) {
       tma_prefetch_map(&a.mapX);
+      tma_prefetch_map(&a.mapXs);
       tma_prefetch_map(&a.mapL);
       tma_prefetch_map(&a.mapS);
     }
@@ -414,8 +521,9 @@ __global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdA
         if (use > 0) mbar_wait(&emptyX[sl], (use - 1) & 1);
         if (TMA) {
           if (lane == 0) {
-            mbar_arrive_expect_tx(&fullX[sl], TILE_BYTES);
-            tma_load_2d(ringX + sl * TILE, &a.mapX, (int)row0, xc * 64, &fullX[sl]);
+            mbar_arrive_expect_tx(&fullX[sl], XSLOT * 8);
+            for (int t = 0; t < 4; ++t)
+              tma_load_2d(ringX + sl * XSLOT + t * 1024, &a.mapX, (int)(row0 + 16 * t), xc * 64, &fullX[sl]);
           }
         } else {
           produce_tile<TR, LDT, false, 64>(ringX + sl * TILE, a.X, a.ldx, row0, a.m, xc * 64, a.q, lane);
@@ -467,6 +575,12 @@ __global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdA
   for (int i = 0; i < 10; ++i) g[i] = 0.0;
   UpdState st;
   const int nch = nmine * nxc;
+  if (TMA) {
+    for (int ch = 0; ch < nch; ++ch) upd_chunk_tma(c, st, ch, accA, g);
+    if (lane == 0) bulk_wait0();
+    if (fuse_gram) gram_blocks_store(a.gram_part + (int64_t)blockIdx.x * 4096, warp, c.gid, c.tig, g);
+    return;
+  }
   for (int ch = 0; ch < nch; ch += 2) {
     upd_chunk(c, st, ch, accA, accB, g);
     if (ch + 1 < nch) upd_chunk(c, st, ch + 1, accB, accA, g);

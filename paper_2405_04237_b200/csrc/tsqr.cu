@@ -116,14 +116,16 @@ tsqr_status tma_encoder() {
 // column-major FP64 matrix (rows x cols, leading dimension ld) as a 2-D tensor map with a
 // (box_rows x box_cols) box; out-of-bounds elements read as zero
 tsqr_status make_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
-                     int box_cols) {
+                     int box_cols, bool swizzle128 = false) {
   TRY(tma_encoder());
   cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(rows, 1), (cuuint64_t)std::max<int64_t>(cols, 1)};
   cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
   cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
   cuuint32_t es[2] = {1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_err("cuTensorMapEncodeTiled failed (%d) rows=%lld cols=%lld ld=%lld", (int)r, (long long)rows,
@@ -293,7 +295,8 @@ struct Launcher {
     const int grid = kSMs;
     const bool tma = tma_ok(X, ldx, m) && tma_ok(L, ldl, m) && tma_ok(S, lds, p);
     if (tma) {
-      TRY(make_map(&a.mapX, X, m, q, ldx, LDT, 64));
+      TRY(make_map(&a.mapX, X, m, q, ldx, 16, 64, true));
+      TRY(make_map(&a.mapXs, X, m, q, ldx, 16, 16, true));
       TRY(make_map(&a.mapL, L, m, p, ldl, LDT, 64));
       TRY(make_map(&a.mapS, S, p, q, lds, LDT, 64));
     }
