@@ -23,7 +23,7 @@ TSQR_OK, TSQR_ERR_INVALID_ARG, TSQR_ERR_UNSUPPORTED, TSQR_ERR_CUDA = 0, 1, 2, 3
 TSQR_ERR_NCCL, TSQR_ERR_BREAKDOWN, TSQR_ERR_WORKSPACE = 4, 5, 6
 KCLASSES = ["gram", "proj", "update", "trmm", "chol", "small", "allreduce"]
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("TSQR_LIB", _build.LIB)  # override: timing experiments only
 
 #: every function declared in include/tsqr.h
 EXPORTS = ["tsqr_workspace_bytes", "tsqr_create", "tsqr_factor", "tsqr_wait", "tsqr_last_counts",

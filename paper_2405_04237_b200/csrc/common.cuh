@@ -91,6 +91,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int 
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void tma_prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -192,12 +193,18 @@ __device__ __forceinline__ void gram_tile_blocks(const double* sm, int warp, int
     ao[u] = (bi * 8 + gid) * LDT + tig;
     bo[u] = (bj * 8 + gid) * LDT + tig;
   }
-  const bool has5 = warp + 32 < 36;
+  if (warp + 32 < 36) {  // warp-uniform: no predicated DMMAs (they would occupy the pipe)
 #pragma unroll 4
-  for (int k0 = 0; k0 < 64; k0 += 4) {
+    for (int k0 = 0; k0 < 64; k0 += 4) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) dmma(g[2 * u], g[2 * u + 1], sm[ao[u] + k0], sm[bo[u] + k0]);
-    if (has5) dmma(g[8], g[9], sm[ao[4] + k0], sm[bo[4] + k0]);
+      for (int u = 0; u < 5; ++u) dmma(g[2 * u], g[2 * u + 1], sm[ao[u] + k0], sm[bo[u] + k0]);
+    }
+  } else {
+#pragma unroll 4
+    for (int k0 = 0; k0 < 64; k0 += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dmma(g[2 * u], g[2 * u + 1], sm[ao[u] + k0], sm[bo[u] + k0]);
+    }
   }
 }
 

@@ -42,6 +42,12 @@ __global__ void k_reduce(const double* __restrict__ part, int S, int p, int q, i
 // -----------------------------------------------------------------------------------------
 constexpr int CHOL_NT = 512;
 
+// shared-memory bytes of k_chol_inv for block size b (S and Z with padded leading dimension
+// b + 1 so that row- and column-wise accesses are bank-conflict free)
+__host__ __device__ constexpr size_t chol_smem_bytes(int b) {
+  return b <= 64 ? sizeof(double) * 2 * (size_t)b * (b + 1) : (b <= 128 ? sizeof(double) * (size_t)b * (b + 1) : 0);
+}
+
 __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restrict__ W, int ldw, int b,
                                                         double* __restrict__ U, int ldu, double* __restrict__ Z,
                                                         int ldz, int* status, int pass, int panel, int stage,
@@ -52,16 +58,20 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restric
   const int tid = threadIdx.x;
   const bool s_in_smem = b <= 128;
   const bool z_in_smem = b <= 64;
-  double* S = s_in_smem ? smem : work;                     // S[i + j*b]
-  double* Zw = z_in_smem ? smem + b * b : Z;                // Zw[i + j*ldzw]
-  const int ldzw = z_in_smem ? b : ldz;
+  const int lds = s_in_smem ? b + 1 : b;
+  double* S = s_in_smem ? smem : work;                          // S[i + j*lds]
+  double* Zw = z_in_smem ? smem + (size_t)b * (b + 1) : Z;      // Zw[i + j*ldzw]
+  const int ldzw = z_in_smem ? b + 1 : ldz;
   for (int e = tid; e < b * b; e += CHOL_NT) {
     const int i = e % b, j = e / b;
-    S[e] = (i <= j) ? W[i + (int64_t)j * ldw] : 0.0;
+    S[i + j * lds] = (i <= j) ? W[i + (int64_t)j * ldw] : 0.0;
   }
   __syncthreads();
+  // right-looking Cholesky (R-5).  Thread -> column jj = tid % 64 (+64 per pass),
+  // rows ii0 = tid / 64 (mod 8): no integer division in the trailing update.
+  const int jj = tid & 63, ii0 = tid >> 6;
   for (int k = 0; k < b; ++k) {
-    const double d = S[k + k * b];
+    const double d = S[k + k * lds];
     if (!(d > 0.0) || !isfinite(d)) {
       if (tid == 0) {
         status[1] = pass; status[2] = panel; status[3] = stage; status[4] = k;
@@ -72,23 +82,26 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restric
       return;  // uniform: every thread read the same d
     }
     const double ukk = sqrt(d);
-    for (int j = k + tid; j < b; j += CHOL_NT) s_urow[j] = (j == k) ? ukk : S[k + j * b] / ukk;
+    for (int j = k + tid; j < b; j += CHOL_NT) s_urow[j] = (j == k) ? ukk : S[k + j * lds] / ukk;
     __syncthreads();
-    for (int j = k + tid; j < b; j += CHOL_NT) S[k + j * b] = s_urow[j];
-    const int nrem = b - k - 1;
-    for (int e = tid; e < nrem * nrem; e += CHOL_NT) {
-      const int i = k + 1 + e % nrem, j = k + 1 + e / nrem;
-      if (i <= j) S[i + j * b] = fma(-s_urow[i], s_urow[j], S[i + j * b]);
+    for (int j0 = 0; j0 < b; j0 += 64) {
+      const int j = j0 + jj;
+      if (j < b && j >= k) {
+        if (ii0 == 0) S[k + j * lds] = s_urow[j];
+        const double uj = s_urow[j];
+        for (int i = k + 1 + ((ii0 - (k + 1)) & 7); i <= j; i += 8) S[i + j * lds] = fma(-s_urow[i], uj, S[i + j * lds]);
+      }
     }
     __syncthreads();
   }
   for (int e = tid; e < b * b; e += CHOL_NT) {
     const int i = e % b, j = e / b;
-    U[i + (int64_t)j * ldu] = (i <= j) ? S[e] : 0.0;
+    U[i + (int64_t)j * ldu] = (i <= j) ? S[i + j * lds] : 0.0;
     Zw[i + (int64_t)j * ldzw] = 0.0;
   }
   __syncthreads();
-  // Z = U^{-1}: rows from the bottom; column j handled by 8 lanes (t-range split 8 ways)
+  // Z = U^{-1} (R-4): rows from the bottom, Z_ij = (delta_ij - sum_{t=i+1..j} U_it Z_tj) / U_ii for
+  // all j >= i in parallel; column j handled by 8 lanes of one warp (the t-range split 8 ways)
   const int sub = tid & 7, jg = tid >> 3;
   for (int i = b - 1; i >= 0; --i) {
     for (int jb = 0; jb < b; jb += CHOL_NT / 8) {  // uniform trip count: shuffles stay converged
@@ -96,18 +109,18 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restric
       const bool act = j < b && j >= i;
       double s = 0.0;
       if (act)
-        for (int t = i + 1 + sub; t <= j; t += 8) s = fma(S[i + t * b], Zw[t + (int64_t)j * ldzw], s);
+        for (int t = i + 1 + sub; t <= j; t += 8) s = fma(S[i + t * lds], Zw[t + (int64_t)j * ldzw], s);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
       s += __shfl_xor_sync(0xffffffffu, s, 4);
-      if (sub == 0 && act) Zw[i + (int64_t)j * ldzw] = (((i == j) ? 1.0 : 0.0) - s) / S[i + i * b];
+      if (sub == 0 && act) Zw[i + (int64_t)j * ldzw] = (((i == j) ? 1.0 : 0.0) - s) / S[i + i * lds];
     }
     __syncthreads();
   }
   if (z_in_smem)
     for (int e = tid; e < b * b; e += CHOL_NT) {
       const int i = e % b, j = e / b;
-      Z[i + (int64_t)j * ldz] = Zw[e];
+      Z[i + (int64_t)j * ldz] = Zw[i + j * ldzw];
     }
 }
 

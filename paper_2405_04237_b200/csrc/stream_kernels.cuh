@@ -457,13 +457,20 @@ __device__ __forceinline__ void upd_chunk_tma(const UpdCtx& c, UpdState& s, int 
       ao[v] = bi * 8 + c.gid;
       bo[v] = bj * 8 + c.gid;
     }
-    const bool has5 = c.warp + 32 < 36;
+    if (c.warp + 32 < 36) {  // warp-uniform: no predicated DMMAs
 #pragma unroll 2
-    for (int k0 = 0; k0 < 64; k0 += 4) {
-      const int r = k0 + c.tig;
+      for (int k0 = 0; k0 < 64; k0 += 4) {
+        const int r = k0 + c.tig;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
-      if (has5) dmma(g[8], g[9], sX[xs_idx(ao[4], r)], sX[xs_idx(bo[4], r)]);
+        for (int v = 0; v < 5; ++v) dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
+      }
+    } else {
+#pragma unroll 2
+      for (int k0 = 0; k0 < 64; k0 += 4) {
+        const int r = k0 + c.tig;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
+      }
     }
   }
   if (c.lane == 0) bulk_wait_read0();  // the TMA stores have read the slot
@@ -611,15 +618,28 @@ struct TrmmCfg {
   static constexpr int RB = TRR / 8 / ROW_GROUPS;
   static constexpr bool ZSMEM = (B <= 64);
   static constexpr int LDZ = B + 4;
-  static constexpr int NS = 3;
+#ifndef TSQR_TRMM_NS
+#define TSQR_TRMM_NS 3
+#endif
+#ifndef TSQR_TRMM_OUT_TMA
+#define TSQR_TRMM_OUT_TMA 1
+#endif
+  static constexpr int NS = (B <= 64) ? TSQR_TRMM_NS : 3;
   static constexpr int BOXC = B < 64 ? B : 64;  // columns per TMA box
   static constexpr int TILE_DBL = B * LD;
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)NS * TILE_DBL + (ZSMEM ? (size_t)B * LDZ : 0)) +
-                                 2 * NS * sizeof(uint64_t) + 128;
+  // TMA-store epilogue (B = 32, 64): 2 output slots of 64 rows x B columns, 128B-swizzled
+  // 16-row boxes; each warp's 8-column blocks are stored by box (16 rows x 8 columns)
+  static constexpr bool OUT_TMA = TSQR_TRMM_OUT_TMA && (B == 32 || B == 64);
+  static constexpr int OUT_DBL = OUT_TMA ? B * 64 : 0;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)2 * OUT_DBL + (size_t)NS * TILE_DBL +
+                                                   (ZSMEM ? (size_t)B * LDZ : 0)) +
+                                 2 * NS * sizeof(uint64_t) + 1024;
 };
 
 struct TrmmArgs {
-  CUtensorMap mapX;  // X: rows m, cols B, box (LD rows, BOXC cols)
+  int exp;            // timing experiments only (0 in production): 1 skip DMMA, 2 skip stores
+  CUtensorMap mapX;   // X: rows m, cols B, box (LD rows, BOXC cols)
+  CUtensorMap mapXs;  // X: rows m, cols B, box (16 rows, 8 cols), 128B swizzle (stores)
   double* X;
   int64_t ldx;
   int64_t m;
@@ -634,9 +654,10 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
   using C = TrmmCfg<B>;
   extern __shared__ __align__(128) double smem_raw[];
   if (failed(a.status)) return;
-  double* smem = aligned_smem(smem_raw);
-  double* ring = smem;
-  double* sZ = smem + C::NS * C::TILE_DBL;
+  double* smem = aligned_smem(smem_raw, 1024);
+  double* outs = smem;                        // 2 swizzled output slots (TMA path, B = 32, 64)
+  double* ring = smem + 2 * C::OUT_DBL;
+  double* sZ = ring + C::NS * C::TILE_DBL;
   uint64_t* full = reinterpret_cast<uint64_t*>(sZ + (C::ZSMEM ? B * C::LDZ : 0));
   uint64_t* empty = full + C::NS;
   double* X = a.X;
@@ -652,7 +673,10 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
       mbar_init(&full[i], TMA ? 1 : 32);
       mbar_init(&empty[i], NCW);
     }
-    if (TMA) tma_prefetch_map(&a.mapX);
+    if (TMA) {
+      tma_prefetch_map(&a.mapX);
+      if (C::OUT_TMA) tma_prefetch_map(&a.mapXs);
+    }
   }
   __syncthreads();
 
@@ -694,9 +718,13 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
     cbs[2 * u] = pr;
     cbs[2 * u + 1] = C::NB - 1 - pr;
   }
-  int maxcb = 0;
+  // the same blocks sorted by their k-bound (ascending): pr_0 < pr_1 < ... < NB-1-pr_1 < NB-1-pr_0
+  int cs[CBW];
 #pragma unroll
-  for (int u = 0; u < CBW; ++u) maxcb = cbs[u] > maxcb ? cbs[u] : maxcb;
+  for (int u = 0; u < C::PAIRS_PER_WARP; ++u) {
+    cs[u] = cbs[2 * u];
+    cs[CBW - 1 - u] = cbs[2 * u + 1];
+  }
   double g[10];
 #pragma unroll
   for (int i = 0; i < 10; ++i) g[i] = 0.0;
@@ -711,15 +739,20 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
     for (int i = 0; i < C::RB; ++i)
 #pragma unroll
       for (int u = 0; u < CBW; ++u) acc[i][u][0] = acc[i][u][1] = 0.0;
-    const int kend = (maxcb + 1) * 8;
-    for (int k0 = 0; k0 < kend; k0 += 4) {
-      double fa[C::RB];
+    // triangular k-loop in phases: in phase ph only the column blocks whose k-range is not yet
+    // exhausted are active (sorted by bound, compile-time active set) -- no predicated DMMAs,
+    // which would still occupy the tensor pipe
+    int k0 = 0;
 #pragma unroll
-      for (int i = 0; i < C::RB; ++i) fa[i] = sX[(k0 + tig) * C::LD + (rg * C::RB + i) * 8 + gid];
+    for (int ph = 0; ph < CBW; ++ph) {
+      const int kend = (a.exp & 1) ? 0 : (cs[ph] + 1) * 8;
+      for (; k0 < kend; k0 += 4) {
+        double fa[C::RB];
 #pragma unroll
-      for (int u = 0; u < CBW; ++u) {
-        if (k0 < (cbs[u] + 1) * 8) {
-          const int col = cbs[u] * 8 + gid;
+        for (int i = 0; i < C::RB; ++i) fa[i] = sX[(k0 + tig) * C::LD + (rg * C::RB + i) * 8 + gid];
+#pragma unroll
+        for (int u = ph; u < CBW; ++u) {
+          const int col = cs[u] * 8 + gid;
           const double fb =
               C::ZSMEM ? sZ[col * C::LDZ + k0 + tig] : __ldg(a.Z + (k0 + tig) + (int64_t)col * a.ldz);
 #pragma unroll
@@ -731,15 +764,48 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
+    if (a.exp & 2) {
+    } else if (TMA && C::OUT_TMA) {
+      // X_new -> swizzled output slot -> TMA box stores (rows past m are clipped)
+      double* so = outs + (it & 1) * C::OUT_DBL;
+      if (it >= 2) {
+        if (lane == 0) bulk_wait_read1();  // this slot's stores from tile it-2 have been read
+        __syncwarp();
+      }
 #pragma unroll
-    for (int i = 0; i < C::RB; ++i) {
-      const int64_t r = row0 + (rg * C::RB + i) * 8 + gid;
-      if (r < m) {
+      for (int i = 0; i < C::RB; ++i) {
+        const int r = (rg * C::RB + i) * 8 + gid;
 #pragma unroll
         for (int u = 0; u < CBW; ++u) {
-          const int c = cbs[u] * 8 + 2 * tig;
-          X[r + (int64_t)c * ldx] = acc[i][u][0];
-          X[r + (int64_t)(c + 1) * ldx] = acc[i][u][1];
+          const int c = cs[u] * 8 + 2 * tig;
+          so[(r >> 4) * (B * 16) + c * 16 + ((((r & 15) >> 1) ^ (c & 7)) << 1) + (r & 1)] = acc[i][u][0];
+          so[(r >> 4) * (B * 16) + (c + 1) * 16 + ((((r & 15) >> 1) ^ ((c + 1) & 7)) << 1) + (r & 1)] =
+              acc[i][u][1];
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int rb = 0; rb < C::RB / 2; ++rb) {
+          const int box = (rg * C::RB) / 2 + rb;
+#pragma unroll
+          for (int u = 0; u < CBW; ++u)
+            tma_store_2d(&a.mapXs, (int)(row0 + 16 * box), cs[u] * 8, so + box * (B * 16) + cs[u] * 8 * 16);
+        }
+        bulk_commit();
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < C::RB; ++i) {
+        const int64_t r = row0 + (rg * C::RB + i) * 8 + gid;
+        if (r < m) {
+#pragma unroll
+          for (int u = 0; u < CBW; ++u) {
+            const int c = cs[u] * 8 + 2 * tig;
+            X[r + (int64_t)c * ldx] = acc[i][u][0];
+            X[r + (int64_t)(c + 1) * ldx] = acc[i][u][1];
+          }
         }
       }
     }
@@ -750,7 +816,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
         const int r = (rg * C::RB + i) * 8 + gid;
 #pragma unroll
         for (int u = 0; u < CBW; ++u) {
-          const int c = cbs[u] * 8 + 2 * tig;
+          const int c = cs[u] * 8 + 2 * tig;
           sX[c * C::LD + r] = acc[i][u][0];
           sX[(c + 1) * C::LD + r] = acc[i][u][1];
         }
@@ -762,6 +828,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
+  if (TMA && C::OUT_TMA && lane == 0) bulk_wait0();
   if (fuse_gram) gram_blocks_store(a.gram_part + (int64_t)blockIdx.x * 4096, warp, gid, tig, g);
 }
 

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -253,8 +254,12 @@ struct Launcher {
     TrmmArgs a;
     std::memset(&a, 0, sizeof(a));
     a.X = X; a.ldx = ldx; a.m = m; a.Z = Z; a.ldz = ldz; a.gram_part = gpart; a.status = status;
+    if (const char* ex = std::getenv("TSQR_EXPERIMENT")) a.exp = std::atoi(ex);  // timing experiments only
     const bool tma = tma_ok(X, ldx, m);
-    if (tma) TRY(make_map(&a.mapX, X, m, B, ldx, C::LD, C::BOXC));
+    if (tma) {
+      TRY(make_map(&a.mapX, X, m, B, ldx, C::LD, C::BOXC));
+      if (C::OUT_TMA) TRY(make_map(&a.mapXs, X, m, B, ldx, 16, 8, true));
+    }
     const size_t t0 = tbegin();
     if (tma) {
       CUDA_TRY(set_smem(k_trmm<B, true>, C::SMEM));
@@ -317,7 +322,7 @@ struct Launcher {
 
   tsqr_status chol_inv(const double* W, int ldw, int b, double* U, int ldu, double* Z, int ldz, int* status_rw,
                        int pass, int panel, int stage, double* work) {
-    const size_t smem = sizeof(double) * (b <= 64 ? 2 * (size_t)b * b : (b <= 128 ? (size_t)b * b : 0));
+    const size_t smem = chol_smem_bytes(b);
     CUDA_TRY(set_smem(k_chol_inv, smem > 0 ? smem : 1));
     const size_t t0 = tbegin();
     k_chol_inv<<<1, CHOL_NT, smem, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage, work);

@@ -45,6 +45,9 @@ def main():
         out[f"update_{p}x{q}"] = {"ms": ms, "tflops": fl / ms / 1e9, "gbs": by / ms / 1e6}
     ms = timeit(lambda: t.trmm(A[:, :64], Z))
     out["trmm_64"] = {"ms": ms, "tflops": m * 64 * 64 / ms / 1e9, "gbs": 16.0 * m * 64 / ms / 1e6}
+    W = t.gram(A[:, :64])
+    ms = timeit(lambda: t.chol_inv(W))
+    out["chol_inv_64"] = {"ms": ms, "tflops": 0.0, "gbs": 0.0}
     ms = timeit(lambda: t.gram(A[:, :64]))
     out["gram_64"] = {"ms": ms, "tflops": m * 64 * 64 / ms / 1e9, "gbs": 8.0 * m * 64 / ms / 1e6}
     for k, v in out.items():
