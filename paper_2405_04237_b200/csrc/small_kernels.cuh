@@ -8,15 +8,17 @@ namespace tsqr {
 // -----------------------------------------------------------------------------------------
 // k_reduce: OUT[i,j] = sum_s PART[s][i,j] in a fixed order (8 interleaved running sums over
 // s, then a pairwise combination) -> deterministic.  gram: only i <= j is read and
-// OUT[j,i] = OUT[i,j] (bitwise symmetric, R-11).  ldp: leading dimension of a partial.
+// OUT[j,i] = OUT[i,j] (bitwise symmetric, R-11); diagonal 64x64 Gram tiles have Sdiag splits,
+// the others Sfull.  ldp: leading dimension of a partial.
 // -----------------------------------------------------------------------------------------
-__global__ void k_reduce(const double* __restrict__ part, int S, int p, int q, int ldp, int64_t pstride,
-                         double* __restrict__ out, int ldo, int gram, const int* status) {
+__global__ void k_reduce(const double* __restrict__ part, int Sfull, int Sdiag, int p, int q, int ldp,
+                         int64_t pstride, double* __restrict__ out, int ldo, int gram, const int* status) {
   if (failed(status)) return;
   const int64_t pq = (int64_t)p * q;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < pq; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e % p), j = (int)(e / p);
     if (gram && i > j) continue;
+    const int S = (gram && (i >> 6) == (j >> 6)) ? Sdiag : Sfull;  // splits of this element's tile
     const double* src = part + i + (int64_t)j * ldp;
     double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int t = 0; t < S; t += 8) {

@@ -51,7 +51,9 @@ struct ProjArgs {
   int p, q;
   int gram;
   int ntp, ntq;
-  int64_t tiles_per_split;
+  int64_t tiles_per_split;       // full tiles
+  int S_full, S_diag;            // row splits of full / diagonal (Gram) tiles
+  int64_t tiles_per_split_diag;
   double* part;  // [S][p*q]
   const int* status;
 };
@@ -99,9 +101,11 @@ __global__ void __launch_bounds__(NTHR, 1) k_proj(const __grid_constant__ ProjAr
   }
   const bool diag = a.gram && ti == tj;
   const int s = blockIdx.y;
+  if (s >= (diag ? a.S_diag : a.S_full)) return;  // this tile type has fewer splits
+  const int64_t tps = diag ? a.tiles_per_split_diag : a.tiles_per_split;
   const int64_t ntr = (a.m + TR - 1) / TR;
-  const int64_t t0 = (int64_t)s * a.tiles_per_split;
-  const int64_t t1 = min(ntr, t0 + a.tiles_per_split);
+  const int64_t t0 = (int64_t)s * tps;
+  const int64_t t1 = min(ntr, t0 + tps);
   const int nt = (int)(t1 > t0 ? t1 - t0 : 0);
   const int pc0 = ti * 64, qc0 = tj * 64;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -613,26 +617,32 @@ struct TrmmCfg {
   static constexpr int PAIRS = NB / 2;
   static constexpr int PAIRS_PER_WARP = PAIRS >= NCW ? PAIRS / NCW : 1;
   static constexpr int ROW_GROUPS = PAIRS >= NCW ? 1 : NCW / PAIRS;
-  static constexpr int TRR = (B <= 64) ? 64 : 32;
+  static constexpr int TRR = (B <= 128) ? 64 : 32;
   static constexpr int LD = TRR + 4;
   static constexpr int RB = TRR / 8 / ROW_GROUPS;
-  static constexpr bool ZSMEM = (B <= 64);
+  // U^{-1} in shared memory: square (B <= 64, ld B + 4) or packed by 8-column block (B = 128:
+  // block cb keeps rows 0..8cb+7 with ld == 4 mod 16, conflict-free B fragments); B = 256
+  // reads it through L1 / L2
+  static constexpr bool ZSMEM = (B <= 128);
+  static constexpr bool ZPACK = (B == 128);
   static constexpr int LDZ = B + 4;
+  __host__ __device__ static constexpr int zld(int cb) { return (8 * (cb + 1)) % 16 == 0 ? 8 * (cb + 1) + 4 : 8 * (cb + 1) + 12; }
+  __host__ __device__ static constexpr int zoff(int cb) { return cb == 0 ? 0 : zoff(cb - 1) + 8 * zld(cb - 1); }
+  static constexpr int ZDBL = ZPACK ? zoff(NB) : (ZSMEM ? B * LDZ : 0);
 #ifndef TSQR_TRMM_NS
 #define TSQR_TRMM_NS 3
 #endif
 #ifndef TSQR_TRMM_OUT_TMA
 #define TSQR_TRMM_OUT_TMA 1
 #endif
-  static constexpr int NS = (B <= 64) ? TSQR_TRMM_NS : 3;
+  static constexpr int NS = (B <= 64) ? TSQR_TRMM_NS : (B == 128 ? 2 : 3);
   static constexpr int BOXC = B < 64 ? B : 64;  // columns per TMA box
   static constexpr int TILE_DBL = B * LD;
   // TMA-store epilogue (B = 32, 64): 2 output slots of 64 rows x B columns, 128B-swizzled
   // 16-row boxes; each warp's 8-column blocks are stored by box (16 rows x 8 columns)
   static constexpr bool OUT_TMA = TSQR_TRMM_OUT_TMA && (B == 32 || B == 64);
   static constexpr int OUT_DBL = OUT_TMA ? B * 64 : 0;
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)2 * OUT_DBL + (size_t)NS * TILE_DBL +
-                                                   (ZSMEM ? (size_t)B * LDZ : 0)) +
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)2 * OUT_DBL + (size_t)NS * TILE_DBL + (size_t)ZDBL) +
                                  2 * NS * sizeof(uint64_t) + 1024;
 };
 
@@ -658,7 +668,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
   double* outs = smem;                        // 2 swizzled output slots (TMA path, B = 32, 64)
   double* ring = smem + 2 * C::OUT_DBL;
   double* sZ = ring + C::NS * C::TILE_DBL;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sZ + (C::ZSMEM ? B * C::LDZ : 0));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sZ + C::ZDBL);
   uint64_t* empty = full + C::NS;
   double* X = a.X;
   const int64_t ldx = a.ldx, m = a.m;
@@ -701,7 +711,13 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
     return;
   }
 
-  if (C::ZSMEM) {
+  if (C::ZPACK) {
+    for (int e = threadIdx.x; e < B * B; e += NCW * 32) {
+      const int k = e % B, col = e / B, cb = col >> 3;
+      if (k < 8 * (cb + 1)) sZ[C::zoff(cb) + (col & 7) * C::zld(cb) + k] = a.Z[k + (int64_t)col * a.ldz];
+    }
+    consumer_sync();
+  } else if (C::ZSMEM) {
     for (int e = threadIdx.x; e < B * B; e += NCW * 32) {
       const int k = e % B, col = e / B;
       sZ[col * C::LDZ + k] = a.Z[k + (int64_t)col * a.ldz];
@@ -753,8 +769,9 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
 #pragma unroll
         for (int u = ph; u < CBW; ++u) {
           const int col = cs[u] * 8 + gid;
-          const double fb =
-              C::ZSMEM ? sZ[col * C::LDZ + k0 + tig] : __ldg(a.Z + (k0 + tig) + (int64_t)col * a.ldz);
+          const double fb = C::ZPACK   ? sZ[C::zoff(cs[u]) + gid * C::zld(cs[u]) + k0 + tig]
+                            : C::ZSMEM ? sZ[col * C::LDZ + k0 + tig]
+                                       : __ldg(a.Z + (k0 + tig) + (int64_t)col * a.ldz);
 #pragma unroll
           for (int i = 0; i < C::RB; ++i) dmma(acc[i][u][0], acc[i][u][1], fa[i], fb);
         }

@@ -68,29 +68,43 @@ bool valid_b(int b) { return b == 16 || b == 32 || b == 64 || b == 128 || b == 2
 
 // ---- split-row policy of k_atb (a function of the problem only -> deterministic) ----
 struct AtbShape {
-  int ntp, ntq, tiles, S;
-  int64_t tps;  // row tiles per split
+  int ntp, ntq, tiles, S;  // S: splits of full tiles
+  int64_t tps;             // row tiles per split (full tiles)
+  int Sd;                  // splits of diagonal Gram tiles
+  int64_t tpsd;
+  int Smax() const { return S > Sd ? S : Sd; }
 };
 
+// splits of `total` row tiles into about `want` parts of equal size (>= 4 row tiles each)
+void split_rows(int64_t ntr, double want, int& S, int64_t& tps) {
+  int64_t s = (int64_t)(want + 1e-9);
+  const int64_t maxS = std::max<int64_t>(1, ntr / 4);
+  s = std::max<int64_t>(1, std::min<int64_t>(s, maxS));
+  tps = std::max<int64_t>(1, (ntr + s - 1) / s);
+  S = (int)std::max<int64_t>(1, (ntr + tps - 1) / tps);
+  if (ntr == 0) S = 1;
+}
+
+// Diagonal Gram tiles cost 576 DMMA per 64-row tile, full tiles 1024: give each tile type
+// its own number of row splits so every CTA carries the same work (~148 CTAs in total).
 AtbShape atb_shape(int64_t m, int p, int q, bool gram) {
   AtbShape s;
   s.ntp = (p + 63) / 64;
   s.ntq = (q + 63) / 64;
-  s.tiles = gram ? s.ntq * (s.ntq + 1) / 2 : s.ntp * s.ntq;
+  const int nd = gram ? s.ntq : 0;                                  // diagonal tiles
+  const int nf = gram ? s.ntq * (s.ntq - 1) / 2 : s.ntp * s.ntq;    // full tiles
+  s.tiles = nd + nf;
   const int64_t ntr = (m + TR - 1) / TR;
-  int S = s.tiles >= kSMs ? 1 : kSMs / s.tiles;
-  const int64_t maxS = std::max<int64_t>(1, ntr / 4);  // >= 4 row tiles per split
-  if (S > maxS) S = (int)maxS;
-  if (S < 1) S = 1;
-  s.tps = std::max<int64_t>(1, (ntr + S - 1) / S);
-  s.S = (int)std::max<int64_t>(1, (ntr + s.tps - 1) / s.tps);
-  if (ntr == 0) s.S = 1;
+  const double wd = 576.0 / 1024.0;
+  const double unit = (double)kSMs / (nd * wd + nf);                // splits per full tile
+  split_rows(ntr, nf ? std::max(1.0, unit) : 1.0, s.S, s.tps);
+  split_rows(ntr, nd ? std::max(1.0, unit * wd) : 1.0, s.Sd, s.tpsd);
   return s;
 }
 
 size_t atb_part_doubles(int64_t m, int p, int q, bool gram) {
   AtbShape s = atb_shape(m, p, q, gram);
-  return (size_t)s.S * (size_t)p * (size_t)q;
+  return (size_t)s.Smax() * (size_t)p * (size_t)q;
 }
 
 int grid_1d(int64_t n, int nt = 256) {
@@ -208,8 +222,9 @@ struct Launcher {
   void tend(size_t e0, int cls, double flops, double bytes) { if (timer) timer->end(st, e0, cls, flops, bytes); }
 
   tsqr_status reduce(const double* part, int S, int p, int q, int ldp, int64_t pstride, double* out, int ldo,
-                     bool gram) {
-    k_reduce<<<grid_1d((int64_t)p * q), 256, 0, st>>>(part, S, p, q, ldp, pstride, out, ldo, gram ? 1 : 0, status);
+                     bool gram, int Sdiag = -1) {
+    k_reduce<<<grid_1d((int64_t)p * q), 256, 0, st>>>(part, S, Sdiag < 0 ? S : Sdiag, p, q, ldp, pstride, out, ldo,
+                                                      gram ? 1 : 0, status);
     CUDA_TRY(cudaGetLastError());
     launches += 1;
     return TSQR_OK;
@@ -223,7 +238,8 @@ struct Launcher {
     std::memset(&a, 0, sizeof(a));
     a.L = L; a.ldl = ldl; a.R = R; a.ldr = ldr; a.m = m; a.p = p; a.q = q; a.gram = gram ? 1 : 0;
     a.ntp = sh.ntp; a.ntq = sh.ntq; a.tiles_per_split = sh.tps; a.part = part; a.status = status;
-    dim3 grid(sh.tiles, sh.S);
+    a.S_full = sh.S; a.S_diag = sh.Sd; a.tiles_per_split_diag = sh.tpsd;
+    dim3 grid(sh.tiles, sh.Smax());
     const bool tma = tma_ok(L, ldl, m) && tma_ok(R, ldr, m);
     if (tma) {
       TRY(make_map(&a.mapL, L, m, p, ldl, LDT, 64));
@@ -239,7 +255,7 @@ struct Launcher {
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
-    TRY(reduce(part, sh.S, p, q, p, (int64_t)p * q, out, ldo, gram));
+    TRY(reduce(part, sh.S, p, q, p, (int64_t)p * q, out, ldo, gram, sh.Sd));
     if (gram) tend(t0, TSQR_KCLASS_GRAM, (double)m * p * p, 8.0 * m * p);
     else tend(t0, TSQR_KCLASS_PROJ, 2.0 * m * p * q, 8.0 * m * (p + q));
     return TSQR_OK;

@@ -45,6 +45,12 @@ def main():
         out[f"update_{p}x{q}"] = {"ms": ms, "tflops": fl / ms / 1e9, "gbs": by / ms / 1e6}
     ms = timeit(lambda: t.trmm(A[:, :64], Z))
     out["trmm_64"] = {"ms": ms, "tflops": m * 64 * 64 / ms / 1e9, "gbs": 16.0 * m * 64 / ms / 1e6}
+    for bb in (128, 256):
+        Zb = torch.triu(torch.randn(bb, bb, dtype=torch.float64, device="cuda")).T.contiguous().T
+        ms = timeit(lambda: t.trmm(A[:, :bb], Zb))
+        out[f"trmm_{bb}"] = {"ms": ms, "tflops": m * bb * bb / ms / 1e9, "gbs": 16.0 * m * bb / ms / 1e6}
+        ms = timeit(lambda: t.gram(A[:, :bb]))
+        out[f"gram_{bb}"] = {"ms": ms, "tflops": m * bb * bb / ms / 1e9, "gbs": 8.0 * m * bb / ms / 1e6}
     W = t.gram(A[:, :64])
     ms = timeit(lambda: t.chol_inv(W))
     out["chol_inv_64"] = {"ms": ms, "tflops": 0.0, "gbs": 0.0}
