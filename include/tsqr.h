@@ -152,7 +152,13 @@ tsqr_status tsqr_timing_reset(tsqr_plan_t plan);
 tsqr_status tsqr_timing(tsqr_plan_t plan, int32_t kclass, double* ms, int64_t* launches, double* flops,
                         double* bytes);
 
-/* Destroy the plan (host state only). */
+/* CUDA graphs (default on): the first tsqr_factor of a plan captures the whole
+ * factorisation (kernels, NCCL allreduces and, if enabled, timing events) into a CUDA graph
+ * that later calls with the same A, lda, R, ldr and timing setting replay with one launch.
+ * enable = 0 switches to eager enqueueing. */
+tsqr_status tsqr_set_graph(tsqr_plan_t plan, int32_t enable);
+
+/* Destroy the plan (host state and its CUDA graph). */
 tsqr_status tsqr_destroy(tsqr_plan_t plan);
 
 /* Human-readable name of a status; static storage. */

@@ -27,7 +27,7 @@ LIB_PATH = os.environ.get("TSQR_LIB", _build.LIB)  # override: timing experiment
 
 #: every function declared in include/tsqr.h
 EXPORTS = ["tsqr_workspace_bytes", "tsqr_create", "tsqr_factor", "tsqr_wait", "tsqr_last_counts",
-           "tsqr_factor_host", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
+           "tsqr_factor_host", "tsqr_set_graph", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
            "tsqr_nccl_comm_init", "tsqr_nccl_comm_destroy", "tsqr_gram", "tsqr_proj", "tsqr_update",
            "tsqr_chol_inv", "tsqr_trmm"]
 
@@ -72,6 +72,7 @@ def load(build_if_missing: bool = False):
     L.tsqr_destroy.argtypes = [_VP]
     L.tsqr_factor_host.argtypes = [_VP, _VP, _I64, _VP, _I32, _VP, _I64, _VP, _I32]
     L.tsqr_set_timing.argtypes = [_VP, _I32]
+    L.tsqr_set_graph.argtypes = [_VP, _I32]
     L.tsqr_timing_reset.argtypes = [_VP]
     L.tsqr_timing.argtypes = [_VP, _I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -211,6 +212,9 @@ class Plan:
         L = load()
         _check(L.tsqr_factor_host(self.handle, A_host.data_ptr(), _ld(A_host), R_host.data_ptr(), _ld(R_host),
                                   A_dev.data_ptr(), _ld(A_dev), R_dev.data_ptr(), _ld(R_dev)), "tsqr_factor_host")
+
+    def set_graph(self, on: bool = True):
+        _check(load().tsqr_set_graph(self.handle, 1 if on else 0), "tsqr_set_graph")
 
     def set_timing(self, on: bool = True):
         _check(load().tsqr_set_timing(self.handle, 1 if on else 0), "tsqr_set_timing")

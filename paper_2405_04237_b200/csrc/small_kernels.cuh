@@ -127,6 +127,158 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restric
 }
 
 // -----------------------------------------------------------------------------------------
+// k_chol_inv_blocked: the same factorisation for b in {128, 256} as a blocked algorithm on
+// 64x64 blocks (one CTA): for each block column J, factor W_JJ (the scalar right-looking
+// kernel above, on a 64x64 block in shared memory) and invert it, form the block row
+// U_JK = U_JJ^{-T} W_JK, and update the trailing blocks W_KL -= U_JK^T U_JL (the blocked form
+// of the same right-looking elimination, R-5).  Then Z = U^{-1} block column by block column:
+// Z_JJ = U_JJ^{-1}, Z_IJ = -Z_II (sum_{K=I+1..J} U_IK Z_KJ) (R-4).  W is copied to the
+// workspace `work` (b x b, L2-resident) and updated there.
+// -----------------------------------------------------------------------------------------
+constexpr int CHB = 64;       // block size
+constexpr int CHLD = 65;      // padded leading dimension in shared memory
+constexpr size_t CHOL_BLK_SMEM = sizeof(double) * 6 * CHB * CHLD;
+
+// C (64x64, ldc) (+)= op(A) * B for 64x64 blocks in shared memory, 512 threads: thread t owns
+// row i = t % 64 and columns c = t / 64 + 8v.  transA: A^T (A[t + i*lda]), else A[i + t*lda].
+// triA: A upper triangular (t restricted to the non-zero range).  sign: +1 / -1.
+template <bool TRANS_A, bool SUB>
+__device__ __forceinline__ void blk_mm(const double* A, const double* B, double* C, int tid) {
+  const int i = tid & 63, c0 = tid >> 6;
+  double acc[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) acc[v] = SUB ? C[i + (c0 + 8 * v) * CHLD] : 0.0;
+  for (int t = 0; t < 64; ++t) {
+    const double a = TRANS_A ? A[t + i * CHLD] : A[i + t * CHLD];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      if (SUB) acc[v] = fma(-a, B[t + (c0 + 8 * v) * CHLD], acc[v]);
+      else acc[v] = fma(a, B[t + (c0 + 8 * v) * CHLD], acc[v]);
+    }
+  }
+  __syncthreads();  // every thread has read A and B (C may alias neither, but callers reuse buffers)
+#pragma unroll
+  for (int v = 0; v < 8; ++v) C[i + (c0 + 8 * v) * CHLD] = acc[v];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void blk_load(double* dst, const double* src, int64_t ld, int tid) {
+  for (int e = tid; e < CHB * CHB; e += CHOL_NT) dst[(e & 63) + (e >> 6) * CHLD] = src[(e & 63) + (int64_t)(e >> 6) * ld];
+  __syncthreads();
+}
+__device__ __forceinline__ void blk_store(double* dst, int64_t ld, const double* src, int tid) {
+  for (int e = tid; e < CHB * CHB; e += CHOL_NT) dst[(e & 63) + (int64_t)(e >> 6) * ld] = src[(e & 63) + (e >> 6) * CHLD];
+  __syncthreads();
+}
+
+// factor the 64x64 block D (upper part valid) in place into U_JJ and write its inverse to Di;
+// returns false (and sets the status) on breakdown
+__device__ bool blk_chol_inv(double* D, double* Di, double* urow, int* status, int pass, int panel, int stage,
+                             int piv0, int tid) {
+  const int jj = tid & 63, ii0 = tid >> 6;
+  for (int k = 0; k < CHB; ++k) {
+    const double d = D[k + k * CHLD];
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (tid == 0) {
+        status[1] = pass; status[2] = panel; status[3] = stage; status[4] = piv0 + k;
+        *reinterpret_cast<double*>(status + 6) = d;
+        __threadfence();
+        status[0] = 5;
+      }
+      return false;
+    }
+    const double ukk = sqrt(d);
+    if (tid >= k && tid < CHB) urow[tid] = (tid == k) ? ukk : D[k + tid * CHLD] / ukk;
+    __syncthreads();
+    if (jj >= k) {
+      if (ii0 == 0) D[k + jj * CHLD] = urow[jj];
+      const double uj = urow[jj];
+      for (int i = k + 1 + ((ii0 - (k + 1)) & 7); i <= jj; i += 8) D[i + jj * CHLD] = fma(-urow[i], uj, D[i + jj * CHLD]);
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < CHB * CHB; e += CHOL_NT) {
+    const int i = e & 63, j = e >> 6;
+    if (i > j) D[i + j * CHLD] = 0.0;
+    Di[i + j * CHLD] = 0.0;
+  }
+  __syncthreads();
+  const int sub = tid & 7, jg = tid >> 3;  // 64 columns x 8 lanes
+  for (int i = CHB - 1; i >= 0; --i) {
+    const int j = jg;
+    const bool act = j >= i;
+    double sacc = 0.0;
+    if (act)
+      for (int t = i + 1 + sub; t <= j; t += 8) sacc = fma(D[i + t * CHLD], Di[t + j * CHLD], sacc);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 4);
+    if (sub == 0 && act) Di[i + j * CHLD] = (((i == j) ? 1.0 : 0.0) - sacc) / D[i + i * CHLD];
+    __syncthreads();
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv_blocked(const double* __restrict__ W, int ldw, int b,
+                                                                double* __restrict__ U, int ldu, double* __restrict__ Z,
+                                                                int ldz, int* status, int pass, int panel, int stage,
+                                                                double* work) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double s_urow[CHB];
+  if (failed(status)) return;
+  const int tid = threadIdx.x;
+  const int nb = b / CHB;
+  double* D = smem;                 // diagonal block -> U_JJ
+  double* Di = smem + CHB * CHLD;   // U_JJ^{-1}
+  double* P = smem + 2 * CHB * CHLD;  // up to 3 panel blocks U_JK
+  double* T = smem + 5 * CHB * CHLD;  // scratch block
+  // work <- upper triangle of W
+  for (int64_t e = tid; e < (int64_t)b * b; e += CHOL_NT) {
+    const int i = (int)(e % b), j = (int)(e / b);
+    work[i + (int64_t)j * b] = (i <= j) ? W[i + (int64_t)j * ldw] : 0.0;
+    U[i + (int64_t)j * ldu] = 0.0;
+    Z[i + (int64_t)j * ldz] = 0.0;
+  }
+  __syncthreads();
+  for (int J = 0; J < nb; ++J) {
+    blk_load(D, work + (int64_t)J * CHB * b + J * CHB, b, tid);
+    if (!blk_chol_inv(D, Di, s_urow, status, pass, panel, stage, J * CHB, tid)) return;
+    blk_store(U + (int64_t)J * CHB * ldu + J * CHB, ldu, D, tid);
+    blk_store(Z + (int64_t)J * CHB * ldz + J * CHB, ldz, Di, tid);
+    // block row: U_JK = U_JJ^{-T} W_JK
+    for (int K = J + 1; K < nb; ++K) {
+      double* PK = P + (K - J - 1) * CHB * CHLD;
+      blk_load(T, work + (int64_t)K * CHB * b + J * CHB, b, tid);
+      blk_mm<true, false>(Di, T, PK, tid);
+      blk_store(U + (int64_t)K * CHB * ldu + J * CHB, ldu, PK, tid);
+    }
+    // trailing update: W_KL -= U_JK^T U_JL, J < K <= L
+    for (int K = J + 1; K < nb; ++K)
+      for (int L2 = K; L2 < nb; ++L2) {
+        double* wkl = work + (int64_t)L2 * CHB * b + K * CHB;
+        blk_load(T, wkl, b, tid);
+        blk_mm<true, true>(P + (K - J - 1) * CHB * CHLD, P + (L2 - J - 1) * CHB * CHLD, T, tid);
+        blk_store(wkl, b, T, tid);
+      }
+  }
+  // Z = U^{-1}: block column J, rows I = J-1 .. 0: Z_IJ = -Z_II * sum_{K=I+1..J} U_IK Z_KJ
+  for (int J = 1; J < nb; ++J)
+    for (int I = J - 1; I >= 0; --I) {
+      for (int e = tid; e < CHB * CHB; e += CHOL_NT) P[(e & 63) + (e >> 6) * CHLD] = 0.0;  // S accumulator
+      __syncthreads();
+      for (int K = I + 1; K <= J; ++K) {
+        blk_load(D, U + (int64_t)K * CHB * ldu + I * CHB, ldu, tid);    // U_IK
+        blk_load(Di, Z + (int64_t)J * CHB * ldz + K * CHB, ldz, tid);   // Z_KJ
+        // P += U_IK Z_KJ  (blk_mm with SUB adds -A*B: accumulate the negative, fixed below)
+        blk_mm<false, true>(D, Di, P, tid);
+      }
+      blk_load(D, Z + (int64_t)I * CHB * ldz + I * CHB, ldz, tid);      // Z_II
+      blk_mm<false, false>(D, P, T, tid);                              // Z_II * (-S) = Z_IJ
+      blk_store(Z + (int64_t)J * CHB * ldz + I * CHB, ldz, T, tid);
+    }
+}
+
+// -----------------------------------------------------------------------------------------
 // R assembly (Alg. 3 l.3 P:185; Alg. 6 l.5/l.8 P:295/P:298; R-8).  Negligible work.
 // -----------------------------------------------------------------------------------------
 // C (n x n) = A * B for upper-triangular A, B: C[i,j] = sum_{t=i..j} A[i,t] B[t,j]; zeros below.

@@ -177,28 +177,40 @@ struct Timer {
   size_t begin(cudaStream_t st) {
     if (!on) return (size_t)-1;
     size_t e = ev();
-    if (e != (size_t)-1) cudaEventRecord(pool[e], st);
+    // External: during stream capture this becomes a timestamped event-record node of the graph
+    if (e != (size_t)-1) cudaEventRecordWithFlags(pool[e], st, capturing ? cudaEventRecordExternal : 0u);
     return e;
   }
   void end(cudaStream_t st, size_t e0, int cls, double flops, double bytes) {
     if (!on || e0 == (size_t)-1) return;
     size_t e1 = ev();
     if (e1 == (size_t)-1) return;
-    cudaEventRecord(pool[e1], st);
+    cudaEventRecordWithFlags(pool[e1], st, capturing ? cudaEventRecordExternal : 0u);
     recs.push_back({cls, e0, e1, flops, bytes});
   }
   // fold recorded events into the totals (events must be complete)
+  // graph mode: `recs` were recorded while capturing a CUDA graph and are re-recorded by every
+  // replay; `pending` counts replays whose events have not been folded in yet
+  bool graph_recs = false;
+  bool capturing = false;  // events are being recorded into a CUDA graph capture
+  int pending = 0;
   void harvest() {
+    if (graph_recs && pending == 0) return;
     for (const Rec& r : recs) {
       float t = 0.f;
       cudaEventElapsedTime(&t, pool[r.e0], pool[r.e1]);
       ms[r.cls] += t; fl[r.cls] += r.flops; by[r.cls] += r.bytes; cnt[r.cls] += 1;
     }
-    recs.clear();
-    used = 0;
+    pending = 0;
+    if (!graph_recs) {
+      recs.clear();
+      used = 0;
+    }
   }
+  void drop_recs() { recs.clear(); used = 0; graph_recs = false; pending = 0; }
   void reset() {
-    recs.clear(); used = 0;
+    if (!graph_recs) { recs.clear(); used = 0; }
+    pending = 0;
     for (int c = 0; c < TSQR_KCLASS_COUNT; ++c) { ms[c] = fl[c] = by[c] = 0; cnt[c] = 0; }
   }
   ~Timer() { for (auto e : pool) cudaEventDestroy(e); }
@@ -338,10 +350,16 @@ struct Launcher {
 
   tsqr_status chol_inv(const double* W, int ldw, int b, double* U, int ldu, double* Z, int ldz, int* status_rw,
                        int pass, int panel, int stage, double* work) {
-    const size_t smem = chol_smem_bytes(b);
-    CUDA_TRY(set_smem(k_chol_inv, smem > 0 ? smem : 1));
     const size_t t0 = tbegin();
-    k_chol_inv<<<1, CHOL_NT, smem, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage, work);
+    if (b >= 128 && b % 64 == 0 && work) {  // blocked variant (64x64 blocks, W staged in `work`)
+      CUDA_TRY(set_smem(k_chol_inv_blocked, CHOL_BLK_SMEM));
+      k_chol_inv_blocked<<<1, CHOL_NT, CHOL_BLK_SMEM, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage,
+                                                            work);
+    } else {
+      const size_t smem = chol_smem_bytes(b);
+      CUDA_TRY(set_smem(k_chol_inv, smem > 0 ? smem : 1));
+      k_chol_inv<<<1, CHOL_NT, smem, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage, work);
+    }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
     tend(t0, TSQR_KCLASS_CHOL, 2.0 * b * b * b / 3.0, 16.0 * b * b);
@@ -398,13 +416,29 @@ struct tsqr_plan_s {
   double* Z = nullptr;       // b x b inverse
   double* R1 = nullptr;      // n x n (CQR2GS pass 1 / CQR2 temporaries)
   double* R2 = nullptr;      // n x n
-  double* cwork = nullptr;   // b x b Cholesky scratch for b > 128
+  double* cwork = nullptr;   // b x b Cholesky scratch (blocked variant, b >= 128)
   double* gpart = nullptr;   // [kGramParts][64*64] fused-Gram partials (b == 64)
   bool fuse = false;         // Gram fused into the update / TRMM epilogues (b == 64)
   Launcher L;
   Timer timer;
   int64_t allreduces = 0;
   tsqr_status sticky = TSQR_OK;
+  // CUDA graph of the whole factorisation, replayed while (A, lda, R, ldr, timing) match
+  bool use_graph = true;
+  cudaStream_t gstream = nullptr;  // non-blocking stream the graph is captured on / replayed on
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  double* gA = nullptr;
+  double* gR = nullptr;
+  int64_t glda = 0;
+  int32_t gldr = 0;
+  bool gtiming = false;
+  ~tsqr_plan_s() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+    if (gstream) cudaStreamDestroy(gstream);
+  }
 };
 
 namespace {
@@ -467,7 +501,7 @@ tsqr_status check_shape(int64_t m_local, int n, int b, tsqr_algo algo) {
 tsqr_status allreduce(tsqr_plan_s* P, double* buf, size_t count) {
   if (P->comm && P->nranks > 1) {
     const size_t t0 = P->L.tbegin();
-    NCCL_TRY(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, P->comm, P->stream));
+    NCCL_TRY(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, P->comm, P->L.st));
     P->L.tend(t0, TSQR_KCLASS_ALLREDUCE, 0.0, 8.0 * count);
     P->allreduces++;
   } else {
@@ -659,18 +693,12 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
   return TSQR_OK;
 }
 
-tsqr_status tsqr_factor(tsqr_plan_t P, double* A, int64_t lda, double* R, int32_t ldr) {
-  if (!P) { set_err("plan == NULL"); return TSQR_ERR_INVALID_ARG; }
-  if ((!A && P->m > 0) || !R || lda < std::max<int64_t>(1, P->m) || ldr < P->n ||
-      (reinterpret_cast<uintptr_t>(A) & 7u) || (reinterpret_cast<uintptr_t>(R) & 7u)) {
-    set_err("bad A/R pointer or leading dimension");
-    return TSQR_ERR_INVALID_ARG;
-  }
+static tsqr_status enqueue_factor(tsqr_plan_t P, double* A, int64_t lda, double* R, int32_t ldr) {
   P->L.launches = 0;
   P->allreduces = 0;
   P->sticky = TSQR_OK;
-  CUDA_TRY(cudaMemsetAsync(P->status, 0, 16 * sizeof(int), P->stream));
-  k_zero2d<<<grid_1d((int64_t)P->n * P->n), 256, 0, P->stream>>>(R, ldr, P->n, P->n);
+  CUDA_TRY(cudaMemsetAsync(P->status, 0, 16 * sizeof(int), P->L.st));
+  k_zero2d<<<grid_1d((int64_t)P->n * P->n), 256, 0, P->L.st>>>(R, ldr, P->n, P->n);
   CUDA_TRY(cudaGetLastError());
   P->L.launches++;
   const int n = P->n, b = P->b;
@@ -690,8 +718,8 @@ tsqr_status tsqr_factor(tsqr_plan_t P, double* A, int64_t lda, double* R, int32_
         s = cqr2_block(P, A, lda, n, R, ldr);
         break;
       }
-      k_zero2d<<<grid_1d((int64_t)n * n), 256, 0, P->stream>>>(P->R1, n, n, n);
-      k_zero2d<<<grid_1d((int64_t)n * n), 256, 0, P->stream>>>(P->R2, n, n, n);
+      k_zero2d<<<grid_1d((int64_t)n * n), 256, 0, P->L.st>>>(P->R1, n, n, n);
+      k_zero2d<<<grid_1d((int64_t)n * n), 256, 0, P->L.st>>>(P->R2, n, n, n);
       P->L.launches += 2;
       s = cqrgs_pass(P, A, lda, P->R1, n, 1);
       if (s == TSQR_OK) s = cqrgs_pass(P, A, lda, P->R2, n, 2);
@@ -702,8 +730,89 @@ tsqr_status tsqr_factor(tsqr_plan_t P, double* A, int64_t lda, double* R, int32_
       break;
   }
   (void)b;
-  P->sticky = s;
   return s;
+}
+
+tsqr_status tsqr_factor(tsqr_plan_t P, double* A, int64_t lda, double* R, int32_t ldr) {
+  if (!P) { set_err("plan == NULL"); return TSQR_ERR_INVALID_ARG; }
+  if ((!A && P->m > 0) || !R || lda < std::max<int64_t>(1, P->m) || ldr < P->n ||
+      (reinterpret_cast<uintptr_t>(A) & 7u) || (reinterpret_cast<uintptr_t>(R) & 7u)) {
+    set_err("bad A/R pointer or leading dimension");
+    return TSQR_ERR_INVALID_ARG;
+  }
+  P->sticky = TSQR_OK;
+  if (P->use_graph && !P->gstream) {
+    if (cudaStreamCreateWithFlags(&P->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+      (void)cudaGetLastError();
+      P->use_graph = false;
+    }
+  }
+  if (!P->use_graph) {
+    if (P->timer.graph_recs) P->timer.drop_recs();
+    P->L.st = P->stream;
+    P->sticky = enqueue_factor(P, A, lda, R, ldr);
+    return P->sticky;
+  }
+  // the graph runs on the plan's own stream, ordered after / before the caller's stream
+  CUDA_TRY(cudaEventRecord(P->ev_in, P->stream));
+  CUDA_TRY(cudaStreamWaitEvent(P->gstream, P->ev_in, 0));
+  const bool same = P->exec && P->gA == A && P->glda == lda && P->gR == R && P->gldr == ldr &&
+                    P->gtiming == P->timer.on;
+  if (!same) {
+    // capture the whole factorisation (kernels, NCCL allreduces, timing events) once
+    if (P->exec) {
+      CUDA_TRY(cudaStreamSynchronize(P->gstream));
+      cudaGraphExecDestroy(P->exec);
+      P->exec = nullptr;
+    }
+    P->timer.drop_recs();
+    CUDA_TRY(cudaStreamBeginCapture(P->gstream, cudaStreamCaptureModeThreadLocal));
+    P->L.st = P->gstream;
+    P->timer.capturing = true;
+    tsqr_status s = enqueue_factor(P, A, lda, R, ldr);
+    P->timer.capturing = false;
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(P->gstream, &g);
+    if (s != TSQR_OK || ce != cudaSuccess || !g) {
+      if (g) cudaGraphDestroy(g);
+      (void)cudaGetLastError();
+      if (s == TSQR_OK) set_err("graph capture failed: %s", cudaGetErrorString(ce));
+      // fall back to eager enqueueing for this plan
+      P->use_graph = false;
+      P->timer.drop_recs();
+      P->L.st = P->stream;
+      P->sticky = enqueue_factor(P, A, lda, R, ldr);
+      return P->sticky;
+    }
+    cudaError_t ie = cudaGraphInstantiate(&P->exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) {
+      P->exec = nullptr;
+      set_err("cudaGraphInstantiate failed: %s", cudaGetErrorString(ie));
+      return TSQR_ERR_CUDA;
+    }
+    P->timer.graph_recs = P->timer.on;
+    P->gA = A; P->glda = lda; P->gR = R; P->gldr = ldr; P->gtiming = P->timer.on;
+  }
+  CUDA_TRY(cudaGraphLaunch(P->exec, P->gstream));
+  CUDA_TRY(cudaEventRecord(P->ev_out, P->gstream));
+  CUDA_TRY(cudaStreamWaitEvent(P->stream, P->ev_out, 0));
+  if (P->timer.on) P->timer.pending++;
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_set_graph(tsqr_plan_t P, int32_t enable) {
+  if (!P) return TSQR_ERR_INVALID_ARG;
+  P->use_graph = enable != 0;
+  if (!P->use_graph && P->exec) {
+    CUDA_TRY(cudaStreamSynchronize(P->gstream));
+    cudaGraphExecDestroy(P->exec);
+    P->exec = nullptr;
+    P->timer.drop_recs();
+  }
+  return TSQR_OK;
 }
 
 tsqr_status tsqr_wait(tsqr_plan_t P, tsqr_breakdown_info* info) {
@@ -712,6 +821,7 @@ tsqr_status tsqr_wait(tsqr_plan_t P, tsqr_breakdown_info* info) {
   int h[16];
   CUDA_TRY(cudaMemcpyAsync(h, P->status, sizeof(h), cudaMemcpyDeviceToHost, P->stream));
   CUDA_TRY(cudaStreamSynchronize(P->stream));
+  if (P->timer.on) P->timer.harvest();  // fold this factorisation's events in before a replay reuses them
   if (P->comm) {
     ncclResult_t async_err = ncclSuccess;
     NCCL_TRY(ncclCommGetAsyncError(P->comm, &async_err));
@@ -868,7 +978,7 @@ tsqr_status tsqr_chol_inv(const double* W, int32_t ldw, int32_t b, double* U, in
   Launcher L;
   L.st = reinterpret_cast<cudaStream_t>(cuda_stream);
   double* work = nullptr;
-  if (b > 128) TRY(scratch((size_t)b * b, L.st, &work));
+  if (b >= 128) TRY(scratch((size_t)b * b, L.st, &work));
   return L.chol_inv(W, ldw, b, U, ldu, Z, ldz, status_dev, 1, 1, 1, work);
 }
 

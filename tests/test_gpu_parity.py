@@ -187,3 +187,50 @@ def test_column_scaling_metamorphic_gpu(T):
     Q1, R1, _ = run_gpu(T, A, 32, "mcqr2gs")
     Q2, R2, _ = run_gpu(T, np.asfortranarray(A * D), 32, "mcqr2gs")
     assert np.array_equal(Q1, Q2) and np.array_equal(R1 * D, R2)
+
+
+def test_graph_replay_and_recapture(T):
+    """The first factor of a plan captures a CUDA graph; later calls with the same buffers
+    replay it (bitwise-identical results), other buffers trigger a re-capture, and eager mode
+    (tsqr_set_graph(0)) gives the same bits."""
+    import torch
+    A, _, _ = synth.generate_np(65536, 256, 1e10, seed=9)
+    p = T.Plan(A.shape[0], 256, 64, "mcqr2gs")
+    outs = []
+    Ad = T.to_colmajor(A)
+    R = T.colmajor_empty(256, 256)
+    for _ in range(3):
+        Ad.copy_(torch.from_numpy(A))
+        p.factor(Ad, R)
+        outs.append((Ad.cpu().numpy(), R.cpu().numpy()))
+    Ad2 = T.to_colmajor(A)
+    R2 = p.factor(Ad2)            # new buffers -> re-capture
+    outs.append((Ad2.cpu().numpy(), R2.cpu().numpy()))
+    p.set_graph(False)
+    Ad3 = T.to_colmajor(A)
+    R3 = p.factor(Ad3)            # eager
+    outs.append((Ad3.cpu().numpy(), R3.cpu().numpy()))
+    for q, r in outs[1:]:
+        assert np.array_equal(q, outs[0][0]) and np.array_equal(r, outs[0][1])
+    assert p.counts()[0] == 4 * 4 - 2
+    p.close()
+
+
+def test_kernel_timing_graph_and_eager(T):
+    """Per-kernel-class CUDA-event timing works both inside the captured graph and eagerly."""
+    import torch
+    A, _, _ = synth.generate_np(65536, 256, 1e8, seed=0)
+    for graph in (True, False):
+        p = T.Plan(65536, 256, 64, "mcqr2gs")
+        p.set_graph(graph)
+        p.set_timing(True)
+        Ad = T.to_colmajor(A)
+        R = T.colmajor_empty(256, 256)
+        for _ in range(3):
+            Ad.copy_(torch.from_numpy(A))
+            p.factor(Ad, R)
+        tm = p.timing()
+        assert tm["update"]["launches"] == 3 * 6 and tm["update"]["ms"] > 0
+        assert tm["proj"]["launches"] == 3 * 6 and tm["proj"]["ms"] > 0
+        assert tm["chol"]["launches"] == 3 * 8
+        p.close()

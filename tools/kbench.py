@@ -49,6 +49,9 @@ def main():
         Zb = torch.triu(torch.randn(bb, bb, dtype=torch.float64, device="cuda")).T.contiguous().T
         ms = timeit(lambda: t.trmm(A[:, :bb], Zb))
         out[f"trmm_{bb}"] = {"ms": ms, "tflops": m * bb * bb / ms / 1e9, "gbs": 16.0 * m * bb / ms / 1e6}
+        Wb = t.gram(A[:, :bb])
+        ms = timeit(lambda: t.chol_inv(Wb))
+        out[f"chol_inv_{bb}"] = {"ms": ms, "tflops": 0.0, "gbs": 0.0}
         ms = timeit(lambda: t.gram(A[:, :bb]))
         out[f"gram_{bb}"] = {"ms": ms, "tflops": m * bb * bb / ms / 1e9, "gbs": 8.0 * m * bb / ms / 1e6}
     W = t.gram(A[:, :64])
