@@ -307,13 +307,14 @@ __global__ void k_gemm_acc_tri(const double* __restrict__ A, int lda, const doub
   }
 }
 
+// D <- alpha S (alpha = +-1 in use: exact)
 __global__ void k_copy2d(const double* __restrict__ S, int64_t lds, double* __restrict__ D, int64_t ldd, int rows,
-                         int cols, const int* status) {
+                         int cols, double alpha, const int* status) {
   if (failed(status)) return;
   const int64_t nn = (int64_t)rows * cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e % rows), j = (int)(e / rows);
-    D[i + j * ldd] = S[i + j * lds];
+    D[i + j * ldd] = alpha * S[i + j * lds];
   }
 }
 

@@ -86,7 +86,9 @@ void split_rows(int64_t ntr, double want, int& S, int64_t& tps) {
 }
 
 // Diagonal Gram tiles cost 576 DMMA per 64-row tile, full tiles 1024: give each tile type
-// its own number of row splits so every CTA carries the same work (~148 CTAs in total).
+// its own number of row splits so every CTA carries the same work.  The split count is then
+// raised (up to 4x) to the value whose CTA count fills whole waves of 148 SMs best (one CTA
+// per SM), e.g. 112 projection tiles -> 5 splits (560 CTAs, 95% of 4 waves) instead of 1.
 AtbShape atb_shape(int64_t m, int p, int q, bool gram) {
   AtbShape s;
   s.ntp = (p + 63) / 64;
@@ -96,7 +98,21 @@ AtbShape atb_shape(int64_t m, int p, int q, bool gram) {
   s.tiles = nd + nf;
   const int64_t ntr = (m + TR - 1) / TR;
   const double wd = 576.0 / 1024.0;
-  const double unit = (double)kSMs / (nd * wd + nf);                // splits per full tile
+  double unit = (double)kSMs / (nd * wd + nf);                      // splits per full tile
+  if (unit < 4.0) {
+    // few splits: choose the multiplier with the best wave efficiency (weighted CTA work)
+    double best_eff = 0.0, best_u = std::max(1.0, unit);
+    for (int f = 1; f <= 16; ++f) {
+      const double u = std::max(1.0, unit) * f / 4.0;
+      if (u < 1.0) continue;
+      const double work = nf * std::floor(u) + nd * std::max(1.0, std::floor(u * wd)) * wd;
+      const double ctas = nf * std::floor(u) + nd * std::max(1.0, std::floor(u * wd));
+      const double waves = std::ceil(ctas / kSMs);
+      const double eff = work / (waves * kSMs);
+      if (eff > best_eff + 1e-3) { best_eff = eff; best_u = u; }
+    }
+    unit = best_u;
+  }
   split_rows(ntr, nf ? std::max(1.0, unit) : 1.0, s.S, s.tps);
   split_rows(ntr, nd ? std::max(1.0, unit * wd) : 1.0, s.Sd, s.tpsd);
   return s;
@@ -316,6 +332,21 @@ struct Launcher {
     }
   }
 
+  // X <- X Z for b = 64 c (c >= 2) by 64-column blocks, last block first (so every block
+  // still reads the old columns to its left):  X_J <- X_J Z_JJ  (64-wide TRMM), then
+  // X_J -= X_{0:J} (-Z_{0:J,J})  (update kernel, Zn = -Z staged in `zwork`, b x b).
+  // Same flops as the direct kernel, but on the two kernels that run near the DMMA roof
+  // instead of the B = 128/256 TRMM whose Z no longer fits shared memory at full width.
+  tsqr_status trmm_blocked(double* X, int64_t ldx, int64_t m, int b, const double* Z, int ldz, double* zwork) {
+    TRY(copy2d(Z, ldz, zwork, b, b, b, -1.0));
+    for (int J = b / 64 - 1; J >= 0; --J) {
+      double* XJ = X + (int64_t)J * 64 * ldx;
+      TRY(trmm_b<64>(XJ, ldx, m, Z + (int64_t)J * 64 + (int64_t)J * 64 * ldz, ldz, nullptr, nullptr));
+      if (J > 0) TRY(update(XJ, ldx, X, ldx, zwork + (int64_t)J * 64 * b, b, m, 64 * J, 64));
+    }
+    return TSQR_OK;
+  }
+
   // X (m x q) -= L (m x p) S (p x q); with gpart (q >= 64): the Gram of the updated first
   // 64 columns, reduced into Wout (64 x 64)
   tsqr_status update(double* X, int64_t ldx, const double* L, int64_t ldl, const double* S, int64_t lds, int64_t m,
@@ -384,9 +415,9 @@ struct Launcher {
     return TSQR_OK;
   }
 
-  tsqr_status copy2d(const double* S, int64_t lds, double* D, int64_t ldd, int rows, int cols) {
+  tsqr_status copy2d(const double* S, int64_t lds, double* D, int64_t ldd, int rows, int cols, double alpha = 1.0) {
     const size_t t0 = tbegin();
-    k_copy2d<<<grid_1d((int64_t)rows * cols), 256, 0, st>>>(S, lds, D, ldd, rows, cols, status);
+    k_copy2d<<<grid_1d((int64_t)rows * cols), 256, 0, st>>>(S, lds, D, ldd, rows, cols, alpha, status);
     CUDA_TRY(cudaGetLastError());
     launches += 1;
     tend(t0, TSQR_KCLASS_SMALL, 0.0, 0.0);
@@ -523,7 +554,10 @@ tsqr_status chol_trmm(tsqr_plan_s* P, double* X, int64_t ldx, int w, double* Uou
                       int stage, bool gram_next) {
   TRY(P->L.chol_inv(P->W, w, w, Uout, ldu, P->Z, w, P->status, pass, panel, stage, P->cwork));
   const bool f = gram_next && P->fuse && w == 64;
-  TRY(P->L.trmm(X, ldx, P->m, w, P->Z, w, f ? P->gpart : nullptr, f ? P->W : nullptr));
+  if (w >= 128 && w % 64 == 0)
+    TRY(P->L.trmm_blocked(X, ldx, P->m, w, P->Z, w, P->cwork));
+  else
+    TRY(P->L.trmm(X, ldx, P->m, w, P->Z, w, f ? P->gpart : nullptr, f ? P->W : nullptr));
   if (f) TRY(allreduce(P, P->W, (size_t)w * w));
   return TSQR_OK;
 }
