@@ -604,6 +604,227 @@ __global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdA
 }
 
 // =========================================================================================
+// k_update_pp: update X -= L S (TMA operands) by two independent consumer warp groups.
+// Each group owns alternate 64-row tiles and walks all 64-column chunks of its tile with its
+// own producer warp, 2-slot ring of 32-wide k halves (L half: [32 cols][68 rows], S half:
+// [64 cols][36 k], both conflict-free for the m8n8k4 fragments) and swizzled X slot.  With
+// GW = 8 warps per group (32x16 warp tiles) every SMSP hosts two warps of each group, so
+// while one group runs its epilogue (X - acc in the slot, TMA stores, optional fused Gram of
+// chunk 0) the other still has two warps per SMSP issuing DMMAs -- one warp per SMSP cannot
+// keep the DMMA pipe full on shared-memory operands (measured ~30 of 37 TF; strict
+// alternation of two 4-warp groups ran at exactly that rate).  Registers are moved from the
+// producer warpgroup to the consumers with setmaxnreg.
+// =========================================================================================
+constexpr int UPP_GW = 8;                                  // warps per consumer group
+constexpr int UPP_NJ = 16 / UPP_GW;                        // 8-column blocks per warp tile
+constexpr int UPP_NTHR = (2 * UPP_GW + 4) * 32;            // + one producer warpgroup
+constexpr int UPP_REG_CONS = UPP_GW == 8 ? 104 : 232;      // setmaxnreg budgets
+constexpr int UPP_REG_PROD = 40;
+constexpr int UPP_LSL = 32 * LDT;          // L half slot (doubles)
+constexpr int UPP_LDS = 36;                // S half slot leading dimension
+constexpr int UPP_SSL = 64 * UPP_LDS;      // S half slot (doubles)
+constexpr uint32_t UPP_TX = (UPP_LSL + UPP_SSL) * 8;
+constexpr int UPP_GROUP = XSLOT + 2 * UPP_LSL + 2 * UPP_SSL;  // doubles per group (multiple of 128)
+constexpr size_t UPP_SMEM = sizeof(double) * 2 * (size_t)UPP_GROUP + 12 * sizeof(uint64_t) + 1024;
+constexpr int UPP_GB = (36 + UPP_GW - 1) / UPP_GW;       // fused-Gram 8x8 blocks per warp (max)
+
+struct UppArgs {
+  CUtensorMap mapX;   // X: box (16 rows, 64 cols), 128-byte swizzle (loads)
+  CUtensorMap mapXs;  // X: box (16 rows, 8*UPP_NJ cols), 128-byte swizzle (stores)
+  CUtensorMap mapL;   // L: box (68 rows, 32 cols)
+  CUtensorMap mapS;   // S: box (36 rows, 64 cols)
+  int64_t m;
+  int p, q;
+  double* gram_part;  // [2 * gridDim.x][64*64] (one partial per warp group) or nullptr
+  const int* status;
+};
+
+__device__ __forceinline__ void group_sync(int grp) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(2 + grp), "n"(UPP_GW * 32) : "memory");
+}
+
+__global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant__ UppArgs a) {
+  extern __shared__ __align__(128) double smem_raw[];
+  if (failed(a.status)) return;
+  double* smem = aligned_smem(smem_raw, 1024);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * UPP_GROUP);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp >= 2 * UPP_GW;
+  const int grp = producer ? (warp - 2 * UPP_GW) & 1 : warp / UPP_GW;
+  double* sX = smem + grp * UPP_GROUP;  // 1024-byte aligned (swizzled slot)
+  double* ringL = sX + XSLOT;
+  double* ringS = ringL + 2 * UPP_LSL;
+  uint64_t* fullLS = bars + grp * 6;
+  uint64_t* emptyLS = fullLS + 2;
+  uint64_t* fullX = fullLS + 4;
+  uint64_t* emptyX = fullLS + 5;
+
+  const int64_t ntr = (a.m + TR - 1) / TR;
+  const int nxc = (a.q + 63) / 64, nkh = (a.p + 31) / 32;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int nmine = (int)(first < ntr ? (ntr - 1 - first) / stride + 1 : 0);
+  const int ntl = nmine > grp ? (nmine - 1 - grp) / 2 + 1 : 0;  // this group's row tiles
+  const int nch = ntl * nxc;
+
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < 2; ++g) {
+      uint64_t* b = bars + g * 6;
+      mbar_init(&b[0], 1); mbar_init(&b[1], 1);            // fullLS
+      mbar_init(&b[2], UPP_GW); mbar_init(&b[3], UPP_GW);  // emptyLS
+      mbar_init(&b[4], 1); mbar_init(&b[5], UPP_GW);       // fullX, emptyX
+    }
+    tma_prefetch_map(&a.mapX);
+    tma_prefetch_map(&a.mapXs);
+    tma_prefetch_map(&a.mapL);
+    tma_prefetch_map(&a.mapS);
+  }
+  __syncthreads();
+
+  if (producer) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(UPP_REG_PROD) : "memory");
+    if (warp >= 2 * UPP_GW + 2 || lane != 0) return;
+    int vLS = 0;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int tl = grp + 2 * (ch / nxc), xc = ch % nxc;
+      const int64_t row0 = (first + (int64_t)tl * stride) * TR;
+      for (int h = 0; h < nkh; ++h, ++vLS) {
+        const int sl = vLS & 1, use = vLS >> 1;
+        if (use > 0) mbar_wait(&emptyLS[sl], (use - 1) & 1);
+        mbar_arrive_expect_tx(&fullLS[sl], UPP_TX);
+        tma_load_2d(ringL + sl * UPP_LSL, &a.mapL, (int)row0, h * 32, &fullLS[sl]);
+        tma_load_2d(ringS + sl * UPP_SSL, &a.mapS, h * 32, xc * 64, &fullLS[sl]);
+      }
+      if (ch > 0) mbar_wait(emptyX, (ch - 1) & 1);
+      mbar_arrive_expect_tx(fullX, XSLOT * 8);
+      for (int t = 0; t < 4; ++t) tma_load_2d(sX + t * 1024, &a.mapX, (int)(row0 + 16 * t), xc * 64, fullX);
+    }
+    return;
+  }
+
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(UPP_REG_CONS) : "memory");
+  const int wg = warp % UPP_GW, wr = wg / (UPP_GW / 2), wc = wg % (UPP_GW / 2);
+  const int gid = lane >> 2, tig = lane & 3;
+  const int c0 = wc * 8 * UPP_NJ;  // first column of this warp's tile within the chunk
+  const bool fuse_gram = a.gram_part != nullptr;
+  double g[2 * UPP_GB];  // fused Gram: this warp's upper 8x8 blocks t = wg + GW v
+#pragma unroll
+  for (int i = 0; i < 2 * UPP_GB; ++i) g[i] = 0.0;
+  const bool full_gb = wg + UPP_GW * (UPP_GB - 1) < 36;  // warp-uniform: no predicated DMMAs
+  int vLS = 0;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int tl = grp + 2 * (ch / nxc), xc = ch % nxc;
+    const int64_t row0 = (first + (int64_t)tl * stride) * TR;
+    double acc[4][UPP_NJ][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < UPP_NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int h = 0; h < nkh; ++h, ++vLS) {
+      const int sl = vLS & 1;
+      mbar_wait(&fullLS[sl], (vLS >> 1) & 1);
+      const double* sL = ringL + sl * UPP_LSL + tig * LDT + wr * 32 + gid;
+      const double* sS = ringS + sl * UPP_SSL + (c0 + gid) * UPP_LDS + tig;
+      // fragments double-buffered in registers: step s+1 is loaded while step s issues
+      double fa[2][4], fb[2][UPP_NJ];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[0][i] = sL[i * 8];
+#pragma unroll
+      for (int j = 0; j < UPP_NJ; ++j) fb[0][j] = sS[j * 8 * UPP_LDS];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int cb = s & 1, nb = cb ^ 1;
+        if (s + 1 < 8) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) fa[nb][i] = sL[(s + 1) * 4 * LDT + i * 8];
+#pragma unroll
+          for (int j = 0; j < UPP_NJ; ++j) fb[nb][j] = sS[j * 8 * UPP_LDS + (s + 1) * 4];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < UPP_NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[cb][i], fb[cb][j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyLS[sl]);
+    }
+    // epilogue: X <- X - acc in the slot (all loads before any store: a store may alias a
+    // later load for the compiler, and interleaving them serialises the load->add->store
+    // chains), then TMA stores of 16 rows x 8*NJ columns per warp
+    mbar_wait(fullX, ch & 1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < UPP_NJ; ++j) {
+        const int r = wr * 32 + i * 8 + gid, col = c0 + j * 8 + 2 * tig;
+        acc[i][j][0] = sX[xs_idx(col, r)] - acc[i][j][0];
+        acc[i][j][1] = sX[xs_idx(col + 1, r)] - acc[i][j][1];
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < UPP_NJ; ++j) {
+        const int r = wr * 32 + i * 8 + gid, col = c0 + j * 8 + 2 * tig;
+        sX[xs_idx(col, r)] = acc[i][j][0];
+        sX[xs_idx(col + 1, r)] = acc[i][j][1];
+      }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int box = 2 * wr + t;
+        tma_store_2d(&a.mapXs, (int)(row0 + 16 * box), xc * 64 + c0, sX + box * 1024 + c0 * 16);
+      }
+      bulk_commit();
+    }
+    if (fuse_gram && xc == 0) {  // Gram of the updated chunk (rows past m are exact zeros)
+      group_sync(grp);
+      int ao[UPP_GB], bo[UPP_GB];
+#pragma unroll
+      for (int v = 0; v < UPP_GB; ++v) {
+        int bi = 0, bj = 0;
+        if (wg + UPP_GW * v < 36) upper_block(wg + UPP_GW * v, bi, bj);
+        ao[v] = bi * 8 + gid;
+        bo[v] = bj * 8 + gid;
+      }
+      if (full_gb) {
+#pragma unroll 2
+        for (int k0 = 0; k0 < 64; k0 += 4) {
+          const int r = k0 + tig;
+#pragma unroll
+          for (int v = 0; v < UPP_GB; ++v) dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
+        }
+      } else {
+#pragma unroll 2
+        for (int k0 = 0; k0 < 64; k0 += 4) {
+          const int r = k0 + tig;
+#pragma unroll
+          for (int v = 0; v < UPP_GB - 1; ++v)
+            dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_read0();  // the TMA stores have read the slot
+    __syncwarp();
+    if (lane == 0) mbar_arrive(emptyX);
+  }
+  if (lane == 0) bulk_wait0();
+  if (fuse_gram) {  // this group's Gram partial (zero if it had no Gram chunk)
+    double* gout = a.gram_part + (int64_t)(2 * blockIdx.x + grp) * 4096;
+#pragma unroll
+    for (int v = 0; v < UPP_GB; ++v) {
+      if (wg + UPP_GW * v < 36) {
+        int bi, bj;
+        upper_block(wg + UPP_GW * v, bi, bj);
+        const int r = bi * 8 + gid, c = bj * 8 + 2 * tig;
+        gout[r + c * 64] = g[2 * v];
+        gout[r + (c + 1) * 64] = g[2 * v + 1];
+      }
+    }
+  }
+}
+
+// =========================================================================================
 // k_trmm: X (m x B) <- X * Z in place, Z upper triangular (B x B): panel orthogonalisation
 // Q = A R^{-1} with the explicit inverse (Alg. 1 l.3 P:133; R-4).  Row tiles are streamed
 // through a 3-stage ring; warp w owns a row group and balanced column-block pairs

@@ -233,7 +233,7 @@ struct Timer {
 };
 
 // ---- kernel launchers (single GPU, enqueue only) ----
-constexpr int kGramParts = kSMs;  // CTAs of the fused-Gram kernels = partials to reduce
+constexpr int kGramParts = 2 * kSMs;  // fused-Gram partials to reduce (k_update_pp: 2 per CTA)
 
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes) {
@@ -352,29 +352,32 @@ struct Launcher {
   tsqr_status update(double* X, int64_t ldx, const double* L, int64_t ldl, const double* S, int64_t lds, int64_t m,
                      int p, int q, double* gpart = nullptr, double* Wout = nullptr) {
     if (q < 64) gpart = nullptr;
-    UpdArgs a;
-    std::memset(&a, 0, sizeof(a));
-    a.X = X; a.ldx = ldx; a.L = L; a.ldl = ldl; a.S = S; a.lds = lds; a.m = m; a.p = p; a.q = q;
-    a.gram_part = gpart; a.status = status;
     const int grid = kSMs;
     const bool tma = tma_ok(X, ldx, m) && tma_ok(L, ldl, m) && tma_ok(S, lds, p);
-    if (tma) {
-      TRY(make_map(&a.mapX, X, m, q, ldx, 16, 64, true));
-      TRY(make_map(&a.mapXs, X, m, q, ldx, 16, 16, true));
-      TRY(make_map(&a.mapL, L, m, p, ldl, LDT, 64));
-      TRY(make_map(&a.mapS, S, p, q, lds, LDT, 64));
-    }
     const size_t t0 = tbegin();
+    int nparts = grid;
     if (tma) {
-      CUDA_TRY(set_smem(k_update<true>, UPD_SMEM));
-      k_update<true><<<grid, NTHR, UPD_SMEM, st>>>(a);
+      UppArgs a;
+      std::memset(&a, 0, sizeof(a));
+      a.m = m; a.p = p; a.q = q; a.gram_part = gpart; a.status = status;
+      TRY(make_map(&a.mapX, X, m, q, ldx, 16, 64, true));
+      TRY(make_map(&a.mapXs, X, m, q, ldx, 16, 8 * UPP_NJ, true));
+      TRY(make_map(&a.mapL, L, m, p, ldl, LDT, 32));
+      TRY(make_map(&a.mapS, S, p, q, lds, UPP_LDS, 64));
+      CUDA_TRY(set_smem(k_update_pp, UPP_SMEM));
+      k_update_pp<<<grid, UPP_NTHR, UPP_SMEM, st>>>(a);
+      nparts = 2 * grid;
     } else {
+      UpdArgs a;
+      std::memset(&a, 0, sizeof(a));
+      a.X = X; a.ldx = ldx; a.L = L; a.ldl = ldl; a.S = S; a.lds = lds; a.m = m; a.p = p; a.q = q;
+      a.gram_part = gpart; a.status = status;
       CUDA_TRY(set_smem(k_update<false>, UPD_SMEM));
       k_update<false><<<grid, NTHR, UPD_SMEM, st>>>(a);
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
-    if (gpart) TRY(reduce(gpart, grid, 64, 64, 64, 4096, Wout, 64, true));
+    if (gpart) TRY(reduce(gpart, nparts, 64, 64, 64, 4096, Wout, 64, true));
     tend(t0, TSQR_KCLASS_UPDATE, 2.0 * m * p * q + (gpart ? 64.0 * 64.0 * m : 0.0), 8.0 * m * (p + 2.0 * q));
     return TSQR_OK;
   }

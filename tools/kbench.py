@@ -12,7 +12,12 @@ sys.path.insert(0, ROOT)
 import paper_2405_04237_b200 as t  # noqa: E402
 
 
-def timeit(fn, reps=7):
+REPS = int(os.environ.get("KB_REPS", 7))
+ONLY = os.environ.get("KB_ONLY", "")
+
+
+def timeit(fn, reps=None):
+    reps = reps or REPS
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     fn()
     torch.cuda.synchronize()
@@ -34,15 +39,17 @@ def main():
     Y = t.colmajor_empty(64, 448); Y.normal_()
     C = t.colmajor_empty(448, 64); C.normal_()
     Z = torch.triu(torch.randn(64, 64, dtype=torch.float64, device="cuda")).T.contiguous().T
-    for (p, q) in [(64, 448), (64, 192), (448, 64), (64, 64)]:
+    for (p, q) in ([] if ONLY and ONLY != "proj" else [(64, 448), (64, 192), (448, 64), (64, 64)]):
         ms = timeit(lambda: t.proj(A[:, :p], A[:, p:p + q]))
         fl, by = 2.0 * m * p * q, 8.0 * m * (p + q)
         out[f"proj_{p}x{q}"] = {"ms": ms, "tflops": fl / ms / 1e9, "gbs": by / ms / 1e6}
-    for (p, q) in [(64, 448), (64, 192), (448, 64), (64, 64)]:
+    for (p, q) in ([] if ONLY and ONLY != "update" else [(64, 448), (64, 256), (64, 128), (64, 64), (128, 64), (256, 64), (448, 64)]):
         S = (Y[:, :q] if p == 64 else C[:p, :q])
         ms = timeit(lambda: t.update(A[:, p:p + q], A[:, :p], S))
         fl, by = 2.0 * m * p * q, 8.0 * m * (p + 2 * q)
         out[f"update_{p}x{q}"] = {"ms": ms, "tflops": fl / ms / 1e9, "gbs": by / ms / 1e6}
+    if ONLY and ONLY not in ("trmm", "misc"):
+        return finish(out)
     ms = timeit(lambda: t.trmm(A[:, :64], Z))
     out["trmm_64"] = {"ms": ms, "tflops": m * 64 * 64 / ms / 1e9, "gbs": 16.0 * m * 64 / ms / 1e6}
     for bb in (128, 256):
@@ -59,6 +66,10 @@ def main():
     out["chol_inv_64"] = {"ms": ms, "tflops": 0.0, "gbs": 0.0}
     ms = timeit(lambda: t.gram(A[:, :64]))
     out["gram_64"] = {"ms": ms, "tflops": m * 64 * 64 / ms / 1e9, "gbs": 8.0 * m * 64 / ms / 1e6}
+    finish(out)
+
+
+def finish(out):
     for k, v in out.items():
         print(f"{k:16s} {v['ms']:8.3f} ms  {v['tflops']:7.2f} TF  {v['gbs']:8.0f} GB/s")
     json.dump(out, open(os.path.join(ROOT, "gpurun_out", "kbench.json"), "w"), indent=1)
