@@ -11,24 +11,39 @@ namespace tsqr {
 // OUT[j,i] = OUT[i,j] (bitwise symmetric, R-11); diagonal 64x64 Gram tiles have Sdiag splits,
 // the others Sfull.  ldp: leading dimension of a partial.
 // -----------------------------------------------------------------------------------------
-__global__ void k_reduce(const double* __restrict__ part, int Sfull, int Sdiag, int p, int q, int ldp,
-                         int64_t pstride, double* __restrict__ out, int ldo, int gram, const int* status) {
+// One CTA of 8 warps per 32 consecutive elements: warp w sums the partials s = w (mod 8) with
+// 4 interleaved running sums, then lane l of warp 0 adds the 8 warp sums pairwise -- a fixed
+// order (deterministic) with 8x the memory parallelism of one thread per element (the fused
+// Gram reductions have 2 x 148 partials).
+constexpr int RED_NT = 256;
+__global__ void __launch_bounds__(RED_NT) k_reduce(const double* __restrict__ part, int Sfull, int Sdiag, int p,
+                                                   int q, int ldp, int64_t pstride, double* __restrict__ out,
+                                                   int ldo, int gram, const int* status) {
   if (failed(status)) return;
+  __shared__ double ws[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pq = (int64_t)p * q;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < pq; e += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t e0 = (int64_t)blockIdx.x * 32; e0 < pq; e0 += (int64_t)gridDim.x * 32) {
+    const int64_t e = e0 + lane;
     const int i = (int)(e % p), j = (int)(e / p);
-    if (gram && i > j) continue;
-    const int S = (gram && (i >> 6) == (j >> 6)) ? Sdiag : Sfull;  // splits of this element's tile
+    const bool live = e < pq && !(gram && i > j);
+    const int S = !live ? 0 : ((gram && (i >> 6) == (j >> 6)) ? Sdiag : Sfull);  // splits of this tile
     const double* src = part + i + (int64_t)j * ldp;
-    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int t = 0; t < S; t += 8) {
+    double s[4] = {0, 0, 0, 0};
+    for (int t = warp; t < S; t += 32) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (t + u < S) s[u] += src[(int64_t)(t + u) * pstride];
+      for (int u = 0; u < 4; ++u)
+        if (t + 8 * u < S) s[u] += src[(int64_t)(t + 8 * u) * pstride];
     }
-    const double v = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
-    out[i + (int64_t)j * ldo] = v;
-    if (gram && i != j) out[j + (int64_t)i * ldo] = v;
+    ws[warp][lane] = (s[0] + s[1]) + (s[2] + s[3]);
+    __syncthreads();
+    if (warp == 0 && live) {
+      const double v = ((ws[0][lane] + ws[1][lane]) + (ws[2][lane] + ws[3][lane])) +
+                       ((ws[4][lane] + ws[5][lane]) + (ws[6][lane] + ws[7][lane]));
+      out[i + (int64_t)j * ldo] = v;
+      if (gram && i != j) out[j + (int64_t)i * ldo] = v;
+    }
+    __syncthreads();
   }
 }
 

@@ -251,8 +251,10 @@ struct Launcher {
 
   tsqr_status reduce(const double* part, int S, int p, int q, int ldp, int64_t pstride, double* out, int ldo,
                      bool gram, int Sdiag = -1) {
-    k_reduce<<<grid_1d((int64_t)p * q), 256, 0, st>>>(part, S, Sdiag < 0 ? S : Sdiag, p, q, ldp, pstride, out, ldo,
-                                                      gram ? 1 : 0, status);
+    const int64_t groups = ((int64_t)p * q + 31) / 32;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, 8 * kSMs));
+    k_reduce<<<grid, RED_NT, 0, st>>>(part, S, Sdiag < 0 ? S : Sdiag, p, q, ldp, pstride, out, ldo, gram ? 1 : 0,
+                                      status);
     CUDA_TRY(cudaGetLastError());
     launches += 1;
     return TSQR_OK;

@@ -19,7 +19,8 @@ src = os.path.join(ROOT, "gpurun_out")
 dst = os.path.join(ROOT, "profiles", tag)
 os.makedirs(dst, exist_ok=True)
 
-CLASS = {"k_update": "update", "k_proj": "proj", "k_trmm": "trmm", "k_chol_inv": "chol", "k_reduce": "reduce"}
+CLASS = {"k_update": "update", "k_update_pp": "update", "k_proj": "proj", "k_trmm": "trmm", "k_chol_inv": "chol",
+         "k_chol_inv_blocked": "chol", "k_reduce": "reduce"}
 
 
 def unit_scale(u):
