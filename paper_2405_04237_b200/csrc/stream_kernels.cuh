@@ -850,25 +850,18 @@ struct TrmmCfg {
   __host__ __device__ static constexpr int zld(int cb) { return (8 * (cb + 1)) % 16 == 0 ? 8 * (cb + 1) + 4 : 8 * (cb + 1) + 12; }
   __host__ __device__ static constexpr int zoff(int cb) { return cb == 0 ? 0 : zoff(cb - 1) + 8 * zld(cb - 1); }
   static constexpr int ZDBL = ZPACK ? zoff(NB) : (ZSMEM ? B * LDZ : 0);
-#ifndef TSQR_TRMM_NS
-#define TSQR_TRMM_NS 3
-#endif
-#ifndef TSQR_TRMM_OUT_TMA
-#define TSQR_TRMM_OUT_TMA 1
-#endif
-  static constexpr int NS = (B <= 64) ? TSQR_TRMM_NS : (B == 128 ? 2 : 3);
+  static constexpr int NS = (B == 128) ? 2 : 3;  // ring stages
   static constexpr int BOXC = B < 64 ? B : 64;  // columns per TMA box
   static constexpr int TILE_DBL = B * LD;
   // TMA-store epilogue (B = 32, 64): 2 output slots of 64 rows x B columns, 128B-swizzled
   // 16-row boxes; each warp's 8-column blocks are stored by box (16 rows x 8 columns)
-  static constexpr bool OUT_TMA = TSQR_TRMM_OUT_TMA && (B == 32 || B == 64);
+  static constexpr bool OUT_TMA = (B == 32 || B == 64);
   static constexpr int OUT_DBL = OUT_TMA ? B * 64 : 0;
   static constexpr size_t SMEM = sizeof(double) * ((size_t)2 * OUT_DBL + (size_t)NS * TILE_DBL + (size_t)ZDBL) +
                                  2 * NS * sizeof(uint64_t) + 1024;
 };
 
 struct TrmmArgs {
-  int exp;            // timing experiments only (0 in production): 1 skip DMMA, 2 skip stores
   CUtensorMap mapX;   // X: rows m, cols B, box (LD rows, BOXC cols)
   CUtensorMap mapXs;  // X: rows m, cols B, box (16 rows, 8 cols), 128B swizzle (stores)
   double* X;
@@ -982,7 +975,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
     int k0 = 0;
 #pragma unroll
     for (int ph = 0; ph < CBW; ++ph) {
-      const int kend = (a.exp & 1) ? 0 : (cs[ph] + 1) * 8;
+      const int kend = (cs[ph] + 1) * 8;
       for (; k0 < kend; k0 += 4) {
         double fa[C::RB];
 #pragma unroll
@@ -1002,8 +995,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
-    if (a.exp & 2) {
-    } else if (TMA && C::OUT_TMA) {
+    if (TMA && C::OUT_TMA) {
       // X_new -> swizzled output slot -> TMA box stores (rows past m are clipped)
       double* so = outs + (it & 1) * C::OUT_DBL;
       if (it >= 2) {

@@ -300,7 +300,6 @@ struct Launcher {
     TrmmArgs a;
     std::memset(&a, 0, sizeof(a));
     a.X = X; a.ldx = ldx; a.m = m; a.Z = Z; a.ldz = ldz; a.gram_part = gpart; a.status = status;
-    if (const char* ex = std::getenv("TSQR_EXPERIMENT")) a.exp = std::atoi(ex);  // timing experiments only
     const bool tma = tma_ok(X, ldx, m);
     if (tma) {
       TRY(make_map(&a.mapX, X, m, B, ldx, C::LD, C::BOXC));
