@@ -217,6 +217,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -256,6 +257,8 @@ def main():
     R = tsqr.colmajor_empty(n, n, device=dev)
     stream = torch.cuda.current_stream(dev)
     plan = tsqr.Plan(m_local, n, b, algo, comm=comm, stream=stream, device=dev)
+    if args.no_graph:
+        plan.set_graph(False)
 
     def barrier():
         if world > 1:
