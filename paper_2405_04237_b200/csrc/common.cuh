@@ -180,48 +180,4 @@ __device__ __forceinline__ void upper_block(int t, int& bi, int& bj) {
   bj = j;
 }
 
-// Fused-epilogue Gram of a 64-row x 64-column tile held in shared memory (sm[c*LDT + r]):
-// warp w owns the upper 8x8 blocks t = w, w+8, ..., < 36 over all 64 rows (16 k-steps), so
-// no cross-warp reduction is needed.  g[10] = up to 5 blocks x 2 accumulators.
-template <int LDT>
-__device__ __forceinline__ void gram_tile_blocks(const double* sm, int warp, int gid, int tig, double (&g)[10]) {
-  int ao[5], bo[5];
-#pragma unroll
-  for (int u = 0; u < 5; ++u) {
-    int bi = 0, bj = 0;
-    if (warp + 8 * u < 36) upper_block(warp + 8 * u, bi, bj);
-    ao[u] = (bi * 8 + gid) * LDT + tig;
-    bo[u] = (bj * 8 + gid) * LDT + tig;
-  }
-  if (warp + 32 < 36) {  // warp-uniform: no predicated DMMAs (they would occupy the pipe)
-#pragma unroll 4
-    for (int k0 = 0; k0 < 64; k0 += 4) {
-#pragma unroll
-      for (int u = 0; u < 5; ++u) dmma(g[2 * u], g[2 * u + 1], sm[ao[u] + k0], sm[bo[u] + k0]);
-    }
-  } else {
-#pragma unroll 4
-    for (int k0 = 0; k0 < 64; k0 += 4) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) dmma(g[2 * u], g[2 * u + 1], sm[ao[u] + k0], sm[bo[u] + k0]);
-    }
-  }
-}
-
-// write the per-warp Gram blocks of gram_tile_blocks to a 64x64 partial (column-major,
-// ld 64); only the upper blocks are written
-__device__ __forceinline__ void gram_blocks_store(double* out, int warp, int gid, int tig, const double (&g)[10]) {
-#pragma unroll
-  for (int u = 0; u < 5; ++u) {
-    const int t = warp + 8 * u;
-    if (t < 36) {
-      int bi, bj;
-      upper_block(t, bi, bj);
-      const int r = bi * 8 + gid, c = bj * 8 + 2 * tig;
-      out[r + c * 64] = g[2 * u];
-      out[r + (c + 1) * 64] = g[2 * u + 1];
-    }
-  }
-}
-
 }  // namespace tsqr

@@ -218,19 +218,14 @@ __global__ void __launch_bounds__(NTHR, 1) k_proj(const __grid_constant__ ProjAr
 }
 
 // =========================================================================================
-// k_update: X (m x q) -= L (m x p) * S (p x q), in place (Alg. 7 l.9 P:351; Alg. 8 l.4
-// P:465 and l.7 P:468).  Work units (row tile, 64-column chunk xc of X, 64-wide k-chunk kc)
-// in order kc < xc < tile; each operand lives in its own 2-slot ring and is re-staged only
-// when it changes (L once per row tile when p <= 64, S once per CTA when p, q <= 64, X once
-// per (tile, xc)).  Consumer warp tile: 32 rows x 16 columns (2 x 4 warp grid); the
-// accumulators hold -X so that -X + L S needs no negation in the inner loop.
-// Optional fused epilogue (gram_part != nullptr, q >= 64): the Gram of the updated first 64
-// columns (the next panel to be factored) accumulated per CTA into gram_part[blockIdx.x]
-// (64x64, upper blocks) -- the panel is not re-read for its CholeskyQR.
+// k_update (fallback for operands without 16-byte TMA strides): X (m x q) -= L (m x p) S,
+// in place (Alg. 7 l.9 P:351; Alg. 8 l.4 P:465 and l.7 P:468).  Work units (row tile, 64-
+// column chunk xc, 64-wide k-chunk kc); one cp.async producer warp stages X, L and S tiles
+// into 2-slot rings; 8 consumer warps with 32x16 warp tiles whose accumulators start from -X.
+// The production path is k_update_pp below.
 // =========================================================================================
 constexpr size_t UPD_SMEM = sizeof(double) * (size_t)6 * TILE + 12 * sizeof(uint64_t) + 1024;
-// TMA path: X slots hold a dense 64x64 tile in four 16-row boxes with the 128-byte swizzle
-constexpr int XSLOT = 64 * 64;
+constexpr int XSLOT = 64 * 64;  // k_update_pp: dense 64x64 X tile in four 16-row swizzled boxes
 
 // double index of element (column c, row r) of a swizzled X slot: box r/16 is [64 cols][16 rows],
 // the 16-byte chunk (r%16)/2 of column c is XORed with c%8 (CU_TENSOR_MAP_SWIZZLE_128B)
@@ -239,10 +234,6 @@ __device__ __forceinline__ int xs_idx(int c, int r) {
 }
 
 struct UpdArgs {
-  CUtensorMap mapX;   // X: rows m, cols q, box (16 rows, 64 cols), 128-byte swizzle (loads)
-  CUtensorMap mapXs;  // X: rows m, cols q, box (16 rows, 16 cols), 128-byte swizzle (stores)
-  CUtensorMap mapL;  // L: rows m, cols p
-  CUtensorMap mapS;  // S: rows p, cols q
   double* X;
   int64_t ldx;
   const double* L;
@@ -251,369 +242,129 @@ struct UpdArgs {
   int64_t lds;
   int64_t m;
   int p, q;
-  double* gram_part;  // [gridDim.x][64*64] or nullptr
   const int* status;
 };
 
-// ---- k_update consumer helpers ----
-struct UpdCtx {
-  const UpdArgs& a;
-  double *ringL, *ringS, *ringX;
-  uint64_t *fullL, *emptyL, *fullS, *emptyS, *fullX, *emptyX;
-  int warp, lane, gid, tig, wr, wc, nxc, nkc;
-  int64_t first, stride;
-  bool fuse_gram;
-};
-struct UpdState {
-  int u = 0, vL = 0, vS = 0, vX = 0;  // unit counter and operand versions (same walk as the producer)
-  bool pend = false;
-  int64_t prow0 = 0;
-  int pxc = 0;
-};
-
-__device__ __forceinline__ bool upd_newL(const UpdCtx& c, int u) { return c.nkc > 1 || (u % c.nxc) == 0; }
-__device__ __forceinline__ bool upd_newS(const UpdCtx& c, int u) { return (c.nkc > 1 || c.nxc > 1) || u == 0; }
-
-// X <- -acc for chunk (row0, xc), straight from the fragments
-__device__ __forceinline__ void upd_store(const UpdCtx& c, int64_t row0, int xc, const double (&acc)[4][2][2]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t r = row0 + c.wr * 32 + i * 8 + c.gid;
-    if (r < c.a.m) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int col = xc * 64 + c.wc * 16 + j * 8 + 2 * c.tig;
-        if (col < c.a.q) c.a.X[r + (int64_t)col * c.a.ldx] = -acc[i][j][0];
-        if (col + 1 < c.a.q) c.a.X[r + (int64_t)(col + 1) * c.a.ldx] = -acc[i][j][1];
-      }
-    }
-  }
-}
-
-// one chunk (tile, xc) = nkc units into `acc`; `other` holds the pending result of the
-// previous chunk (stored after this chunk's first k-chunk)
-__device__ __forceinline__ void upd_chunk(const UpdCtx& c, UpdState& s, int ch, double (&acc)[4][2][2],
-                                          double (&other)[4][2][2], double (&g)[10]) {
-  const int tl = ch / c.nxc, xc = ch % c.nxc;
-  const int64_t row0 = (c.first + (int64_t)tl * c.stride) * TR;
-  const bool gram_here = c.fuse_gram && xc == 0;
-  // accumulators <- -X from the chunk's X slot
-  const int slX = s.vX & 1;
-  mbar_wait(&c.fullX[slX], (s.vX >> 1) & 1);
-  double* sX = c.ringX + slX * TILE;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int r = c.wr * 32 + i * 8 + c.gid, col = c.wc * 16 + j * 8 + 2 * c.tig;
-      acc[i][j][0] = -sX[col * LDT + r];
-      acc[i][j][1] = -sX[(col + 1) * LDT + r];
-    }
-  if (!gram_here) {
-    __syncwarp();
-    if (c.lane == 0) mbar_arrive(&c.emptyX[slX]);
-  }
-  ++s.vX;
-  for (int kc = 0; kc < c.nkc; ++kc, ++s.u) {
-    const int u = s.u;
-    const bool nl = upd_newL(c, u), ns = upd_newS(c, u);
-    const int slL = (s.vL - (nl ? 0 : 1)) & 1;
-    if (nl) {
-      mbar_wait(&c.fullL[slL], (s.vL >> 1) & 1);
-      ++s.vL;
-    }
-    const int slS = (s.vS - (ns ? 0 : 1)) & 1;
-    if (ns) {
-      mbar_wait(&c.fullS[slS], (s.vS >> 1) & 1);
-      ++s.vS;
-    }
-    const double* sL = c.ringL + slL * TILE;
-    const double* sS = c.ringS + slS * TILE;
-    // k beyond p is zero-filled in both L and S: the full 64-wide chunk is exact
-#pragma unroll 4
-    for (int k0 = 0; k0 < 64; k0 += 4) {
-      double fa[4], fb[2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) fa[i] = sL[(k0 + c.tig) * LDT + c.wr * 32 + i * 8 + c.gid];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) fb[j] = sS[(c.wc * 16 + j * 8 + c.gid) * LDT + k0 + c.tig];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
-    }
-    // release L / S when the next unit stages a new version (no release is needed after the
-    // CTA's last unit: the producer has nothing left to stage)
-    __syncwarp();
-    if (c.lane == 0) {
-      if (upd_newL(c, u + 1)) mbar_arrive(&c.emptyL[slL]);
-      if (upd_newS(c, u + 1)) mbar_arrive(&c.emptyS[slS]);
-    }
-    if (kc == 0 && s.pend) {  // the previous chunk's result: its DMMAs have long completed
-      upd_store(c, s.prow0, s.pxc, other);
-      s.pend = false;
-    }
-  }
-  if (gram_here) {
-    upd_store(c, row0, xc, acc);
-    // fused Gram of the updated 64-column chunk: write it back into its X slot (each warp
-    // owns its region), then every warp accumulates its upper 8x8 blocks
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int r = c.wr * 32 + i * 8 + c.gid, col = c.wc * 16 + j * 8 + 2 * c.tig;
-        const bool ok = row0 + r < c.a.m;  // rows past m stay exactly zero
-        sX[col * LDT + r] = ok ? -acc[i][j][0] : 0.0;
-        sX[(col + 1) * LDT + r] = ok ? -acc[i][j][1] : 0.0;
-      }
-    consumer_sync();
-    gram_tile_blocks<LDT>(sX, c.warp, c.gid, c.tig, g);
-    fence_proxy_async();  // generic writes above precede the next TMA fill of this slot
-    __syncwarp();
-    if (c.lane == 0) mbar_arrive(&c.emptyX[slX]);
-  } else {
-    s.pend = true;
-    s.prow0 = row0;
-    s.pxc = xc;
-  }
-}
-
-// TMA-path chunk: -X from the swizzled slot, nkc k-chunks, then -acc written back into the
-// slot and stored by two per-warp TMA boxes (16 rows x 16 columns); the optional fused Gram
-// reads the updated chunk from the same slot.
-__device__ __forceinline__ void upd_chunk_tma(const UpdCtx& c, UpdState& s, int ch, double (&acc)[4][2][2],
-                                              double (&g)[10]) {
-  const int tl = ch / c.nxc, xc = ch % c.nxc;
-  const int64_t row0 = (c.first + (int64_t)tl * c.stride) * TR;
-  const bool gram_here = c.fuse_gram && xc == 0;
-  const int slX = s.vX & 1;
-  mbar_wait(&c.fullX[slX], (s.vX >> 1) & 1);
-  double* sX = c.ringX + slX * XSLOT;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int r = c.wr * 32 + i * 8 + c.gid, col = c.wc * 16 + j * 8 + 2 * c.tig;
-      acc[i][j][0] = -sX[xs_idx(col, r)];
-      acc[i][j][1] = -sX[xs_idx(col + 1, r)];
-    }
-  ++s.vX;
-  for (int kc = 0; kc < c.nkc; ++kc, ++s.u) {
-    const int u = s.u;
-    const bool nl = upd_newL(c, u), ns = upd_newS(c, u);
-    const int slL = (s.vL - (nl ? 0 : 1)) & 1;
-    if (nl) {
-      mbar_wait(&c.fullL[slL], (s.vL >> 1) & 1);
-      ++s.vL;
-    }
-    const int slS = (s.vS - (ns ? 0 : 1)) & 1;
-    if (ns) {
-      mbar_wait(&c.fullS[slS], (s.vS >> 1) & 1);
-      ++s.vS;
-    }
-    const double* sL = c.ringL + slL * TILE;
-    const double* sS = c.ringS + slS * TILE;
-#pragma unroll 4
-    for (int k0 = 0; k0 < 64; k0 += 4) {
-      double fa[4], fb[2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) fa[i] = sL[(k0 + c.tig) * LDT + c.wr * 32 + i * 8 + c.gid];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) fb[j] = sS[(c.wc * 16 + j * 8 + c.gid) * LDT + k0 + c.tig];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
-    }
-    __syncwarp();
-    if (c.lane == 0) {
-      if (upd_newL(c, u + 1)) mbar_arrive(&c.emptyL[slL]);
-      if (upd_newS(c, u + 1)) mbar_arrive(&c.emptyS[slS]);
-    }
-  }
-  // X <- -acc through the slot and two TMA stores per warp
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int r = c.wr * 32 + i * 8 + c.gid, col = c.wc * 16 + j * 8 + 2 * c.tig;
-      sX[xs_idx(col, r)] = -acc[i][j][0];
-      sX[xs_idx(col + 1, r)] = -acc[i][j][1];
-    }
-  fence_proxy_async();
-  __syncwarp();
-  if (c.lane == 0) {
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int box = 2 * c.wr + t;
-      tma_store_2d(&c.a.mapXs, (int)(row0 + 16 * box), xc * 64 + c.wc * 16, sX + box * 1024 + c.wc * 16 * 16);
-    }
-    bulk_commit();
-  }
-  if (gram_here) {
-    consumer_sync();  // every warp's part of the updated chunk is in the slot
-    int ao[5], bo[5];
-#pragma unroll
-    for (int v = 0; v < 5; ++v) {
-      int bi = 0, bj = 0;
-      if (c.warp + 8 * v < 36) upper_block(c.warp + 8 * v, bi, bj);
-      ao[v] = bi * 8 + c.gid;
-      bo[v] = bj * 8 + c.gid;
-    }
-    if (c.warp + 32 < 36) {  // warp-uniform: no predicated DMMAs
-#pragma unroll 2
-      for (int k0 = 0; k0 < 64; k0 += 4) {
-        const int r = k0 + c.tig;
-#pragma unroll
-        for (int v = 0; v < 5; ++v) dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
-      }
-    } else {
-#pragma unroll 2
-      for (int k0 = 0; k0 < 64; k0 += 4) {
-        const int r = k0 + c.tig;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
-      }
-    }
-  }
-  if (c.lane == 0) bulk_wait_read0();  // the TMA stores have read the slot
-  __syncwarp();
-  if (c.lane == 0) mbar_arrive(&c.emptyX[slX]);
-}
-
-template <bool TMA>
 __global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdArgs a) {
   extern __shared__ __align__(128) double smem_raw[];
   if (failed(a.status)) return;
-  double* smem = aligned_smem(smem_raw, 1024);
+  double* smem = aligned_smem(smem_raw, 128);
   double* ringL = smem;             // 2 slots
   double* ringS = smem + 2 * TILE;  // 2 slots
-  double* ringX = smem + 4 * TILE;  // 2 slots (TMA path: 2 swizzled XSLOTs; 4*TILE*8 % 1024 == 0)
+  double* ringX = smem + 4 * TILE;  // 2 slots
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * TILE);
   uint64_t *fullL = bars, *emptyL = bars + 2, *fullS = bars + 4, *emptyS = bars + 6, *fullX = bars + 8,
            *emptyX = bars + 10;
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntr = (a.m + TR - 1) / TR;
   const int nxc = (a.q + 63) / 64, nkc = (a.p + 63) / 64;
   const int64_t first = blockIdx.x, stride = gridDim.x;
   const int nmine = (int)(first < ntr ? (ntr - 1 - first) / stride + 1 : 0);
   const int units = nmine * nxc * nkc;
-  const bool fuse_gram = a.gram_part != nullptr;
-  // which operands change at unit u (same rule on both sides)
-  auto newL = [&](int u) { return nkc > 1 || (u % nxc) == 0; };  // nkc == 1: new row tile
-  auto newS = [&](int u) { return (nkc > 1 || nxc > 1) || u == 0; };
-  auto newX = [&](int u) { return (u % nkc) == 0; };
-
   if (threadIdx.x == 0) {
-    const uint32_t fc = TMA ? 1 : 32;
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&fullL[i], fc); mbar_init(&emptyL[i], NCW);
-      mbar_init(&fullS[i], fc); mbar_init(&emptyS[i], NCW);
-      mbar_init(&fullX[i], fc); mbar_init(&emptyX[i], NCW);
-    }
-    if (TMA) {
-      tma_prefetch_map(&a.mapX);
-      tma_prefetch_map(&a.mapXs);
-      tma_prefetch_map(&a.mapL);
-      tma_prefetch_map(&a.mapS);
+      mbar_init(&fullL[i], 32); mbar_init(&emptyL[i], NCW);
+      mbar_init(&fullS[i], 32); mbar_init(&emptyS[i], NCW);
+      mbar_init(&fullX[i], 32); mbar_init(&emptyX[i], NCW);
     }
   }
   __syncthreads();
-
+  // every unit stages its L and S chunks; X once per (tile, xc) (unit kc == 0)
   if (warp == PRODUCER) {
-    int vL = 0, vS = 0, vX = 0;
     for (int u = 0; u < units; ++u) {
       const int tl = u / (nxc * nkc), rem = u % (nxc * nkc), xc = rem / nkc, kc = rem % nkc;
       const int64_t row0 = (first + (int64_t)tl * stride) * TR;
-      if (newX(u)) {
+      const int vX = u / nkc;
+      if (kc == 0) {
         const int sl = vX & 1, use = vX >> 1;
         if (use > 0) mbar_wait(&emptyX[sl], (use - 1) & 1);
-        if (TMA) {
-          if (lane == 0) {
-            mbar_arrive_expect_tx(&fullX[sl], XSLOT * 8);
-            for (int t = 0; t < 4; ++t)
-              tma_load_2d(ringX + sl * XSLOT + t * 1024, &a.mapX, (int)(row0 + 16 * t), xc * 64, &fullX[sl]);
-          }
-        } else {
-          produce_tile<TR, LDT, false, 64>(ringX + sl * TILE, a.X, a.ldx, row0, a.m, xc * 64, a.q, lane);
-          cp_async_arrive(&fullX[sl]);
-        }
-        ++vX;
+        produce_tile<TR, LDT, false, 64>(ringX + sl * TILE, a.X, a.ldx, row0, a.m, xc * 64, a.q, lane);
+        cp_async_arrive(&fullX[sl]);
       }
-      if (newL(u)) {
-        const int sl = vL & 1, use = vL >> 1;
+      {
+        const int sl = u & 1, use = u >> 1;
         if (use > 0) mbar_wait(&emptyL[sl], (use - 1) & 1);
-        if (TMA) {
-          if (lane == 0) {
-            mbar_arrive_expect_tx(&fullL[sl], TILE_BYTES);
-            tma_load_2d(ringL + sl * TILE, &a.mapL, (int)row0, kc * 64, &fullL[sl]);
-          }
-        } else {
-          produce_tile<TR, LDT, false, 64>(ringL + sl * TILE, a.L, a.ldl, row0, a.m, kc * 64, a.p, lane);
-          cp_async_arrive(&fullL[sl]);
-        }
-        ++vL;
-      }
-      if (newS(u)) {
-        const int sl = vS & 1, use = vS >> 1;
+        produce_tile<TR, LDT, false, 64>(ringL + sl * TILE, a.L, a.ldl, row0, a.m, kc * 64, a.p, lane);
+        cp_async_arrive(&fullL[sl]);
         if (use > 0) mbar_wait(&emptyS[sl], (use - 1) & 1);
-        // S chunk (kc, xc): rows (k) kc*64.., columns xc*64.. of the p x q matrix S
-        if (TMA) {
-          if (lane == 0) {
-            mbar_arrive_expect_tx(&fullS[sl], TILE_BYTES);
-            tma_load_2d(ringS + sl * TILE, &a.mapS, kc * 64, xc * 64, &fullS[sl]);
-          }
-        } else {
-          produce_tile<64, LDT, false, 64>(ringS + sl * TILE, a.S, a.lds, (int64_t)kc * 64, a.p, xc * 64, a.q, lane);
-          cp_async_arrive(&fullS[sl]);
-        }
-        ++vS;
+        produce_tile<64, LDT, false, 64>(ringS + sl * TILE, a.S, a.lds, (int64_t)kc * 64, a.p, xc * 64, a.q, lane);
+        cp_async_arrive(&fullS[sl]);
       }
     }
     return;
   }
-
-  // Consumers walk the chunks (tile, xc) with two accumulator sets: the result of chunk c
-  // stays "pending" and is stored only after chunk c+1's first k-chunk has been issued, so
-  // the accumulator drain never stalls the DMMA pipe (gram chunks are finished in place).
-  UpdCtx c{a, ringL, ringS, ringX, fullL, emptyL, fullS, emptyS, fullX, emptyX, warp, lane, lane >> 2, lane & 3,
-           warp >> 2, warp & 3, nxc, nkc, first, stride, fuse_gram};
-  double accA[4][2][2], accB[4][2][2];
-  double g[10];
+  const int gid = lane >> 2, tig = lane & 3, wr = warp >> 2, wc = warp & 3;
+  double acc[4][2][2];
+  for (int u = 0; u < units; ++u) {
+    const int tl = u / (nxc * nkc), rem = u % (nxc * nkc), xc = rem / nkc, kc = rem % nkc;
+    const int64_t row0 = (first + (int64_t)tl * stride) * TR;
+    const int vX = u / nkc;
+    if (kc == 0) {  // accumulators <- -X
+      const int sl = vX & 1;
+      mbar_wait(&fullX[sl], (vX >> 1) & 1);
+      const double* sX = ringX + sl * TILE;
 #pragma unroll
-  for (int i = 0; i < 10; ++i) g[i] = 0.0;
-  UpdState st;
-  const int nch = nmine * nxc;
-  if (TMA) {
-    for (int ch = 0; ch < nch; ++ch) upd_chunk_tma(c, st, ch, accA, g);
-    if (lane == 0) bulk_wait0();
-    if (fuse_gram) gram_blocks_store(a.gram_part + (int64_t)blockIdx.x * 4096, warp, c.gid, c.tig, g);
-    return;
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int r = wr * 32 + i * 8 + gid, col = wc * 16 + j * 8 + 2 * tig;
+          acc[i][j][0] = -sX[col * LDT + r];
+          acc[i][j][1] = -sX[(col + 1) * LDT + r];
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyX[sl]);
+    }
+    const int sl = u & 1;
+    mbar_wait(&fullL[sl], (u >> 1) & 1);
+    mbar_wait(&fullS[sl], (u >> 1) & 1);
+    const double* sL = ringL + sl * TILE;
+    const double* sS = ringS + sl * TILE;
+    // k beyond p is zero-filled in both L and S: the full 64-wide chunk is exact
+#pragma unroll 4
+    for (int k0 = 0; k0 < 64; k0 += 4) {
+      double fa[4], fb[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) fa[i] = sL[(k0 + tig) * LDT + wr * 32 + i * 8 + gid];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) fb[j] = sS[(wc * 16 + j * 8 + gid) * LDT + k0 + tig];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&emptyL[sl]);
+      mbar_arrive(&emptyS[sl]);
+    }
+    if (kc == nkc - 1) {  // X <- -acc
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t r = row0 + wr * 32 + i * 8 + gid;
+        if (r < a.m) {
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int col = xc * 64 + wc * 16 + j * 8 + 2 * tig;
+            if (col < a.q) a.X[r + (int64_t)col * a.ldx] = -acc[i][j][0];
+            if (col + 1 < a.q) a.X[r + (int64_t)(col + 1) * a.ldx] = -acc[i][j][1];
+          }
+        }
+      }
+    }
   }
-  for (int ch = 0; ch < nch; ch += 2) {
-    upd_chunk(c, st, ch, accA, accB, g);
-    if (ch + 1 < nch) upd_chunk(c, st, ch + 1, accB, accA, g);
-  }
-  if (st.pend) {  // the last chunk (index nch-1) used accA when nch-1 is even
-    if (((nch - 1) & 1) == 0) upd_store(c, st.prow0, st.pxc, accA);
-    else upd_store(c, st.prow0, st.pxc, accB);
-  }
-  if (fuse_gram) gram_blocks_store(a.gram_part + (int64_t)blockIdx.x * 4096, warp, c.gid, c.tig, g);
 }
 
 // =========================================================================================
-// k_update_pp: update X -= L S (TMA operands) by two independent consumer warp groups.
-// Each group owns alternate 64-row tiles and walks all 64-column chunks of its tile with its
-// own producer warp, 2-slot ring of 32-wide k halves (L half: [32 cols][68 rows], S half:
-// [64 cols][36 k], both conflict-free for the m8n8k4 fragments) and swizzled X slot.  With
-// GW = 8 warps per group (32x16 warp tiles) every SMSP hosts two warps of each group, so
-// while one group runs its epilogue (X - acc in the slot, TMA stores, optional fused Gram of
-// chunk 0) the other still has two warps per SMSP issuing DMMAs -- one warp per SMSP cannot
-// keep the DMMA pipe full on shared-memory operands (measured ~30 of 37 TF; strict
-// alternation of two 4-warp groups ran at exactly that rate).  Registers are moved from the
-// producer warpgroup to the consumers with setmaxnreg.
+// k_update_pp: update X -= L S (TMA operands; Alg. 7 l.9 P:351, Alg. 8 l.4 P:465 and l.7
+// P:468) by two independent consumer warp groups.  Each group owns alternate 64-row tiles and
+// walks all 64-column chunks of its tile with its own producer warp, 2-slot ring of 32-wide k
+// halves (L half: [32 cols][68 rows], S half: [64 cols][36 k], both conflict-free for the
+// m8n8k4 fragments) and swizzled X slot (TMA load in, X - acc written back in place, TMA
+// stores out).  With GW = 8 warps per group (32x16 warp tiles) every SMSP hosts two warps of
+// each group, so while one group runs its epilogue the other still has two warps per SMSP
+// issuing DMMAs -- one warp per SMSP cannot keep the DMMA pipe full on shared-memory operands
+// (measured ~30 of 37 TF; strict alternation of two 4-warp groups ran at exactly that rate).
+// Registers are moved from the producer warpgroup to the consumers with setmaxnreg.
 // =========================================================================================
 constexpr int UPP_GW = 8;                                  // warps per consumer group
 constexpr int UPP_NJ = 16 / UPP_GW;                        // 8-column blocks per warp tile
@@ -626,7 +377,6 @@ constexpr int UPP_SSL = 64 * UPP_LDS;      // S half slot (doubles)
 constexpr uint32_t UPP_TX = (UPP_LSL + UPP_SSL) * 8;
 constexpr int UPP_GROUP = XSLOT + 2 * UPP_LSL + 2 * UPP_SSL;  // doubles per group (multiple of 128)
 constexpr size_t UPP_SMEM = sizeof(double) * 2 * (size_t)UPP_GROUP + 12 * sizeof(uint64_t) + 1024;
-constexpr int UPP_GB = (36 + UPP_GW - 1) / UPP_GW;       // fused-Gram 8x8 blocks per warp (max)
 
 struct UppArgs {
   CUtensorMap mapX;   // X: box (16 rows, 64 cols), 128-byte swizzle (loads)
@@ -635,13 +385,8 @@ struct UppArgs {
   CUtensorMap mapS;   // S: box (36 rows, 64 cols)
   int64_t m;
   int p, q;
-  double* gram_part;  // [2 * gridDim.x][64*64] (one partial per warp group) or nullptr
   const int* status;
 };
-
-__device__ __forceinline__ void group_sync(int grp) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(2 + grp), "n"(UPP_GW * 32) : "memory");
-}
 
 __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant__ UppArgs a) {
   extern __shared__ __align__(128) double smem_raw[];
@@ -705,11 +450,6 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
   const int wg = warp % UPP_GW, wr = wg / (UPP_GW / 2), wc = wg % (UPP_GW / 2);
   const int gid = lane >> 2, tig = lane & 3;
   const int c0 = wc * 8 * UPP_NJ;  // first column of this warp's tile within the chunk
-  const bool fuse_gram = a.gram_part != nullptr;
-  double g[2 * UPP_GB];  // fused Gram: this warp's upper 8x8 blocks t = wg + GW v
-#pragma unroll
-  for (int i = 0; i < 2 * UPP_GB; ++i) g[i] = 0.0;
-  const bool full_gb = wg + UPP_GW * (UPP_GB - 1) < 36;  // warp-uniform: no predicated DMMAs
   int vLS = 0;
   for (int ch = 0; ch < nch; ++ch) {
     const int tl = grp + 2 * (ch / nxc), xc = ch % nxc;
@@ -777,51 +517,11 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
       }
       bulk_commit();
     }
-    if (fuse_gram && xc == 0) {  // Gram of the updated chunk (rows past m are exact zeros)
-      group_sync(grp);
-      int ao[UPP_GB], bo[UPP_GB];
-#pragma unroll
-      for (int v = 0; v < UPP_GB; ++v) {
-        int bi = 0, bj = 0;
-        if (wg + UPP_GW * v < 36) upper_block(wg + UPP_GW * v, bi, bj);
-        ao[v] = bi * 8 + gid;
-        bo[v] = bj * 8 + gid;
-      }
-      if (full_gb) {
-#pragma unroll 2
-        for (int k0 = 0; k0 < 64; k0 += 4) {
-          const int r = k0 + tig;
-#pragma unroll
-          for (int v = 0; v < UPP_GB; ++v) dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
-        }
-      } else {
-#pragma unroll 2
-        for (int k0 = 0; k0 < 64; k0 += 4) {
-          const int r = k0 + tig;
-#pragma unroll
-          for (int v = 0; v < UPP_GB - 1; ++v)
-            dmma(g[2 * v], g[2 * v + 1], sX[xs_idx(ao[v], r)], sX[xs_idx(bo[v], r)]);
-        }
-      }
-    }
     if (lane == 0) bulk_wait_read0();  // the TMA stores have read the slot
     __syncwarp();
     if (lane == 0) mbar_arrive(emptyX);
   }
   if (lane == 0) bulk_wait0();
-  if (fuse_gram) {  // this group's Gram partial (zero if it had no Gram chunk)
-    double* gout = a.gram_part + (int64_t)(2 * blockIdx.x + grp) * 4096;
-#pragma unroll
-    for (int v = 0; v < UPP_GB; ++v) {
-      if (wg + UPP_GW * v < 36) {
-        int bi, bj;
-        upper_block(wg + UPP_GW * v, bi, bj);
-        const int r = bi * 8 + gid, c = bj * 8 + 2 * tig;
-        gout[r + c * 64] = g[2 * v];
-        gout[r + (c + 1) * 64] = g[2 * v + 1];
-      }
-    }
-  }
 }
 
 // =========================================================================================
@@ -829,8 +529,7 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
 // Q = A R^{-1} with the explicit inverse (Alg. 1 l.3 P:133; R-4).  Row tiles are streamed
 // through a 3-stage ring; warp w owns a row group and balanced column-block pairs
 // (cb, NB-1-cb) so the triangular work is even.  Z is in shared memory for B <= 64, read
-// through L1/L2 otherwise.  Optional fused epilogue (B == 64, gram_part != nullptr): Gram
-// of the new tile (the next CholeskyQR's Gram, Alg. 3 l.2) per CTA.
+// through L1/L2 otherwise (b >= 128 panels use the blocked 64-wide TRMM + update path).
 // =========================================================================================
 template <int B>
 struct TrmmCfg {
@@ -869,7 +568,6 @@ struct TrmmArgs {
   int64_t m;
   const double* Z;
   int ldz;
-  double* gram_part;
   const int* status;
 };
 
@@ -890,7 +588,6 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
   const int64_t ntr = (m + C::TRR - 1) / C::TRR;
   const int64_t first = blockIdx.x, stride = gridDim.x;
   const int nmine = (int)(first < ntr ? (ntr - 1 - first) / stride + 1 : 0);
-  const bool fuse_gram = (B == 64) && a.gram_part != nullptr;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NS; ++i) {
@@ -955,9 +652,6 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
     cs[u] = cbs[2 * u];
     cs[CBW - 1 - u] = cbs[2 * u + 1];
   }
-  double g[10];
-#pragma unroll
-  for (int i = 0; i < 10; ++i) g[i] = 0.0;
 
   for (int it = 0; it < nmine; ++it) {
     const int st = it % C::NS;
@@ -991,10 +685,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
         }
       }
     }
-    if (!fuse_gram) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
     if (TMA && C::OUT_TMA) {
       // X_new -> swizzled output slot -> TMA box stores (rows past m are clipped)
       double* so = outs + (it & 1) * C::OUT_DBL;
@@ -1039,27 +731,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_trmm(const __grid_constant__ TrmmAr
         }
       }
     }
-    if (fuse_gram) {
-      consumer_sync();  // every warp has finished reading the old tile
-#pragma unroll
-      for (int i = 0; i < C::RB; ++i) {
-        const int r = (rg * C::RB + i) * 8 + gid;
-#pragma unroll
-        for (int u = 0; u < CBW; ++u) {
-          const int c = cs[u] * 8 + 2 * tig;
-          sX[c * C::LD + r] = acc[i][u][0];
-          sX[(c + 1) * C::LD + r] = acc[i][u][1];
-        }
-      }
-      consumer_sync();
-      gram_tile_blocks<C::LD>(sX, warp, gid, tig, g);
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-    }
   }
   if (TMA && C::OUT_TMA && lane == 0) bulk_wait0();
-  if (fuse_gram) gram_blocks_store(a.gram_part + (int64_t)blockIdx.x * 4096, warp, gid, tig, g);
 }
 
 }  // namespace tsqr

@@ -233,7 +233,6 @@ struct Timer {
 };
 
 // ---- kernel launchers (single GPU, enqueue only) ----
-constexpr int kGramParts = 2 * kSMs;  // fused-Gram partials to reduce (k_update_pp: 2 per CTA)
 
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes) {
@@ -291,15 +290,14 @@ struct Launcher {
     return TSQR_OK;
   }
 
-  // X <- X Z (in place); with gpart != nullptr (B == 64 only) also the per-CTA Gram of the
-  // result into gpart[kGramParts][64*64], reduced into Wout
+  // X <- X Z (in place)
   template <int B>
-  tsqr_status trmm_b(double* X, int64_t ldx, int64_t m, const double* Z, int ldz, double* gpart, double* Wout) {
+  tsqr_status trmm_b(double* X, int64_t ldx, int64_t m, const double* Z, int ldz) {
     using C = TrmmCfg<B>;
     const int grid = kSMs;
     TrmmArgs a;
     std::memset(&a, 0, sizeof(a));
-    a.X = X; a.ldx = ldx; a.m = m; a.Z = Z; a.ldz = ldz; a.gram_part = gpart; a.status = status;
+    a.X = X; a.ldx = ldx; a.m = m; a.Z = Z; a.ldz = ldz; a.status = status;
     const bool tma = tma_ok(X, ldx, m);
     if (tma) {
       TRY(make_map(&a.mapX, X, m, B, ldx, C::LD, C::BOXC));
@@ -315,20 +313,17 @@ struct Launcher {
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
-    if (gpart) TRY(reduce(gpart, grid, B, B, 64, 4096, Wout, B, true));
-    tend(t0, TSQR_KCLASS_TRMM, (double)m * B * B + (gpart ? (double)m * B * B : 0.0), 16.0 * m * B);
+    tend(t0, TSQR_KCLASS_TRMM, (double)m * B * B, 16.0 * m * B);
     return TSQR_OK;
   }
 
-  tsqr_status trmm(double* X, int64_t ldx, int64_t m, int b, const double* Z, int ldz, double* gpart = nullptr,
-                   double* Wout = nullptr) {
-    if (b != 64) gpart = nullptr;
+  tsqr_status trmm(double* X, int64_t ldx, int64_t m, int b, const double* Z, int ldz) {
     switch (b) {
-      case 16: return trmm_b<16>(X, ldx, m, Z, ldz, nullptr, nullptr);
-      case 32: return trmm_b<32>(X, ldx, m, Z, ldz, nullptr, nullptr);
-      case 64: return trmm_b<64>(X, ldx, m, Z, ldz, gpart, Wout);
-      case 128: return trmm_b<128>(X, ldx, m, Z, ldz, nullptr, nullptr);
-      case 256: return trmm_b<256>(X, ldx, m, Z, ldz, nullptr, nullptr);
+      case 16: return trmm_b<16>(X, ldx, m, Z, ldz);
+      case 32: return trmm_b<32>(X, ldx, m, Z, ldz);
+      case 64: return trmm_b<64>(X, ldx, m, Z, ldz);
+      case 128: return trmm_b<128>(X, ldx, m, Z, ldz);
+      case 256: return trmm_b<256>(X, ldx, m, Z, ldz);
       default: set_err("trmm: unsupported b=%d", b); return TSQR_ERR_UNSUPPORTED;
     }
   }
@@ -342,44 +337,39 @@ struct Launcher {
     TRY(copy2d(Z, ldz, zwork, b, b, b, -1.0));
     for (int J = b / 64 - 1; J >= 0; --J) {
       double* XJ = X + (int64_t)J * 64 * ldx;
-      TRY(trmm_b<64>(XJ, ldx, m, Z + (int64_t)J * 64 + (int64_t)J * 64 * ldz, ldz, nullptr, nullptr));
+      TRY(trmm_b<64>(XJ, ldx, m, Z + (int64_t)J * 64 + (int64_t)J * 64 * ldz, ldz));
       if (J > 0) TRY(update(XJ, ldx, X, ldx, zwork + (int64_t)J * 64 * b, b, m, 64 * J, 64));
     }
     return TSQR_OK;
   }
 
-  // X (m x q) -= L (m x p) S (p x q); with gpart (q >= 64): the Gram of the updated first
-  // 64 columns, reduced into Wout (64 x 64)
+  // X (m x q) -= L (m x p) S (p x q)
   tsqr_status update(double* X, int64_t ldx, const double* L, int64_t ldl, const double* S, int64_t lds, int64_t m,
-                     int p, int q, double* gpart = nullptr, double* Wout = nullptr) {
-    if (q < 64) gpart = nullptr;
+                     int p, int q) {
     const int grid = kSMs;
     const bool tma = tma_ok(X, ldx, m) && tma_ok(L, ldl, m) && tma_ok(S, lds, p);
     const size_t t0 = tbegin();
-    int nparts = grid;
     if (tma) {
       UppArgs a;
       std::memset(&a, 0, sizeof(a));
-      a.m = m; a.p = p; a.q = q; a.gram_part = gpart; a.status = status;
+      a.m = m; a.p = p; a.q = q; a.status = status;
       TRY(make_map(&a.mapX, X, m, q, ldx, 16, 64, true));
       TRY(make_map(&a.mapXs, X, m, q, ldx, 16, 8 * UPP_NJ, true));
       TRY(make_map(&a.mapL, L, m, p, ldl, LDT, 32));
       TRY(make_map(&a.mapS, S, p, q, lds, UPP_LDS, 64));
       CUDA_TRY(set_smem(k_update_pp, UPP_SMEM));
       k_update_pp<<<grid, UPP_NTHR, UPP_SMEM, st>>>(a);
-      nparts = 2 * grid;
     } else {
       UpdArgs a;
       std::memset(&a, 0, sizeof(a));
       a.X = X; a.ldx = ldx; a.L = L; a.ldl = ldl; a.S = S; a.lds = lds; a.m = m; a.p = p; a.q = q;
-      a.gram_part = gpart; a.status = status;
-      CUDA_TRY(set_smem(k_update<false>, UPD_SMEM));
-      k_update<false><<<grid, NTHR, UPD_SMEM, st>>>(a);
+      a.status = status;
+      CUDA_TRY(set_smem(k_update, UPD_SMEM));
+      k_update<<<grid, NTHR, UPD_SMEM, st>>>(a);
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
-    if (gpart) TRY(reduce(gpart, nparts, 64, 64, 64, 4096, Wout, 64, true));
-    tend(t0, TSQR_KCLASS_UPDATE, 2.0 * m * p * q + (gpart ? 64.0 * 64.0 * m : 0.0), 8.0 * m * (p + 2.0 * q));
+    tend(t0, TSQR_KCLASS_UPDATE, 2.0 * m * p * q, 8.0 * m * (p + 2.0 * q));
     return TSQR_OK;
   }
 
@@ -452,8 +442,6 @@ struct tsqr_plan_s {
   double* R1 = nullptr;      // n x n (CQR2GS pass 1 / CQR2 temporaries)
   double* R2 = nullptr;      // n x n
   double* cwork = nullptr;   // b x b Cholesky scratch (blocked variant, b >= 128)
-  double* gpart = nullptr;   // [kGramParts][64*64] fused-Gram partials (b == 64)
-  bool fuse = false;         // Gram fused into the update / TRMM epilogues (b == 64)
   Launcher L;
   Timer timer;
   int64_t allreduces = 0;
@@ -515,10 +503,9 @@ size_t carve(Carve& c, tsqr_plan_s* p, int64_t m, int n, int b, tsqr_algo algo) 
   double* R1 = c.take<double>((size_t)n * n);
   double* R2 = c.take<double>((size_t)n * n);
   double* cw = c.take<double>((size_t)b * b);
-  double* gp = c.take<double>(b == 64 ? (size_t)kGramParts * 4096 : 1);
   if (p) {
     p->status = status; p->part = part; p->W = W; p->Y = Y; p->U1 = U1; p->U2 = U2; p->Z = Z;
-    p->R1 = R1; p->R2 = R2; p->cwork = cw; p->gpart = gp;
+    p->R1 = R1; p->R2 = R2; p->cwork = cw;
   }
   return align_up(c.off);
 }
@@ -551,25 +538,22 @@ tsqr_status gram(tsqr_plan_s* P, const double* X, int64_t ldx, int w) {
   return allreduce(P, P->W, (size_t)w * w);
 }
 
-// Cholesky + inverse of the (already allreduced) Gram W, then X <- X U^{-1}.  With
-// gram_next the TRMM epilogue also forms the Gram of the new X and allreduces it into W
-// (the next CholeskyQR's Gram, fused: saves re-reading the panel).
+// Cholesky + inverse of the (already allreduced) Gram W, then X <- X U^{-1}.
+// (Every Gram is a standalone split-row kernel.  Fusing the next Gram into the TRMM / update
+// epilogues saves one read of the panel, but on B200 the fused epilogue Gram ran at about half
+// the DMMA efficiency of the standalone kernel and stalled the update's main loop: measured
+// at cfg3, fused 149.7 ms/step vs standalone 146.3 ms/step on the same GPU.)
 tsqr_status chol_trmm(tsqr_plan_s* P, double* X, int64_t ldx, int w, double* Uout, int ldu, int pass, int panel,
-                      int stage, bool gram_next) {
+                      int stage) {
   TRY(P->L.chol_inv(P->W, w, w, Uout, ldu, P->Z, w, P->status, pass, panel, stage, P->cwork));
-  const bool f = gram_next && P->fuse && w == 64;
-  if (w >= 128 && w % 64 == 0)
-    TRY(P->L.trmm_blocked(X, ldx, P->m, w, P->Z, w, P->cwork));
-  else
-    TRY(P->L.trmm(X, ldx, P->m, w, P->Z, w, f ? P->gpart : nullptr, f ? P->W : nullptr));
-  if (f) TRY(allreduce(P, P->W, (size_t)w * w));
-  return TSQR_OK;
+  if (w >= 128 && w % 64 == 0) return P->L.trmm_blocked(X, ldx, P->m, w, P->Z, w, P->cwork);
+  return P->L.trmm(X, ldx, P->m, w, P->Z, w);
 }
 
 // CholeskyQR of the m x w slab X in place (Alg. 2): U -> Uout (ldu), X <- X U^{-1}
 tsqr_status cqr(tsqr_plan_s* P, double* X, int64_t ldx, int w, double* Uout, int ldu, int pass, int panel, int stage) {
   TRY(gram(P, X, ldx, w));
-  return chol_trmm(P, X, ldx, w, Uout, ldu, pass, panel, stage, false);
+  return chol_trmm(P, X, ldx, w, Uout, ldu, pass, panel, stage);
 }
 
 // OUT (p x q, ld p) <- allreduce(L^T Rm)
@@ -578,40 +562,34 @@ tsqr_status proj(tsqr_plan_s* P, const double* Lm, int64_t ldl, int p, const dou
   return allreduce(P, out, (size_t)p * q);
 }
 
-// X (m x q) -= L S; with gram_next (fused path) also W <- allreduce(Gram of X's first 64 columns)
+// X (m x q) -= L S (row-local: no communication)
 tsqr_status update(tsqr_plan_s* P, double* X, int64_t ldx, const double* Lm, int64_t ldl, const double* S, int lds,
-                   int p, int q, bool gram_next) {
-  const bool f = gram_next && P->fuse && q >= 64;
-  TRY(P->L.update(X, ldx, Lm, ldl, S, lds, P->m, p, q, f ? P->gpart : nullptr, f ? P->W : nullptr));
-  if (f) TRY(allreduce(P, P->W, (size_t)64 * 64));
-  return TSQR_OK;
+                   int p, int q) {
+  return P->L.update(X, ldx, Lm, ldl, S, lds, P->m, p, q);
 }
 
 // CQR2 of the first b columns (Alg. 3; Alg. 8 l.1): U1, U2 -> R_11 = U2 U1
 tsqr_status cqr2_block(tsqr_plan_s* P, double* A, int64_t lda, int w, double* R, int ldr) {
   TRY(gram(P, A, lda, w));
-  TRY(chol_trmm(P, A, lda, w, P->U1, w, 1, 1, 1, true));
-  if (!(P->fuse && w == 64)) TRY(gram(P, A, lda, w));
-  TRY(chol_trmm(P, A, lda, w, P->U2, w, 1, 1, 2, false));
+  TRY(chol_trmm(P, A, lda, w, P->U1, w, 1, 1, 1));
+  TRY(gram(P, A, lda, w));
+  TRY(chol_trmm(P, A, lda, w, P->U2, w, 1, 1, 2));
   return P->L.trimul(P->U2, w, P->U1, w, R, ldr, w);
 }
 
 // one CQRGS pass (Alg. 7) writing its R into Rp (ld ldr)
 tsqr_status cqrgs_pass(tsqr_plan_s* P, double* A, int64_t lda, double* Rp, int ldr, int pass) {
   const int n = P->n, b = P->b, k = P->k;
-  bool have_gram = false;  // W already holds the Gram of panel j (fused into the previous update)
   for (int j = 0; j < k; ++j) {
     double* Aj = A + (int64_t)j * b * lda;
-    if (!have_gram) TRY(gram(P, Aj, lda, b));                                  // l.2-3
+    TRY(gram(P, Aj, lda, b));                                                  // l.2-3
     // l.4-6: R_jj = U (the Cholesky writes straight into R's diagonal block)
-    TRY(chol_trmm(P, Aj, lda, b, Rp + (int64_t)j * b + (int64_t)j * b * ldr, ldr, pass, j + 1, 1, false));
+    TRY(chol_trmm(P, Aj, lda, b, Rp + (int64_t)j * b + (int64_t)j * b * ldr, ldr, pass, j + 1, 1));
     const int nt = n - (j + 1) * b;
-    have_gram = false;
     if (nt > 0) {
       double* At = A + (int64_t)(j + 1) * b * lda;
       TRY(proj(P, Aj, lda, b, At, lda, nt, P->Y));                            // l.7-8
-      TRY(update(P, At, lda, Aj, lda, P->Y, b, b, nt, true));                 // l.9 (+ Gram of A_{j+1})
-      have_gram = P->fuse;
+      TRY(update(P, At, lda, Aj, lda, P->Y, b, b, nt));                       // l.9
       TRY(P->L.copy2d(P->Y, b, Rp + (int64_t)j * b + (int64_t)(j + 1) * b * ldr, ldr, b, nt));  // l.10
     }
   }
@@ -625,20 +603,20 @@ tsqr_status run_mcqr2gs(tsqr_plan_s* P, double* A, int64_t lda, double* R, int l
     double* Ap = A + (int64_t)(j - 1) * b * lda;  // Q_{j-1}
     double* Aj = A + (int64_t)j * b * lda;
     const int Nj = n - j * b;
-    // l.3-5: Y = Q_{j-1}^T A_{:,j:k}; A_{:,j:k} -= Q_{j-1} Y (+ Gram of A_j); R_{j-1,j:k} = Y
+    // l.3-5: Y = Q_{j-1}^T A_{:,j:k}; A_{:,j:k} -= Q_{j-1} Y; R_{j-1,j:k} = Y
     TRY(proj(P, Ap, lda, b, Aj, lda, Nj, P->Y));
-    TRY(update(P, Aj, lda, Ap, lda, P->Y, b, b, Nj, true));
+    TRY(update(P, Aj, lda, Ap, lda, P->Y, b, b, Nj));
     TRY(P->L.copy2d(P->Y, b, R + (int64_t)(j - 1) * b + (int64_t)j * b * ldr, ldr, b, Nj));
     // l.6: first CQR, panel -> V1, keep U1
-    if (!P->fuse) TRY(gram(P, Aj, lda, b));
-    TRY(chol_trmm(P, Aj, lda, b, P->U1, b, 1, j + 1, 1, false));
-    // l.7: C = Q_{1:j-1}^T V1 ((j-1)b x b); V1 -= Q_{1:j-1} C (+ Gram of V1')
+    TRY(gram(P, Aj, lda, b));
+    TRY(chol_trmm(P, Aj, lda, b, P->U1, b, 1, j + 1, 1));
+    // l.7: C = Q_{1:j-1}^T V1 ((j-1)b x b); V1 -= Q_{1:j-1} C
     const int jb = j * b;
     TRY(proj(P, A, lda, jb, Aj, lda, b, P->Y));
-    TRY(update(P, Aj, lda, A, lda, P->Y, jb, jb, b, true));
+    TRY(update(P, Aj, lda, A, lda, P->Y, jb, jb, b));
     // l.8: second CQR -> Q_j, U2
-    if (!P->fuse) TRY(gram(P, Aj, lda, b));
-    TRY(chol_trmm(P, Aj, lda, b, P->U2, b, 1, j + 1, 2, false));
+    TRY(gram(P, Aj, lda, b));
+    TRY(chol_trmm(P, Aj, lda, b, P->U2, b, 1, j + 1, 2));
     // R_jj = U2 U1; R_{1:j-1,j} += C U1  (R-8)
     TRY(P->L.trimul(P->U2, b, P->U1, b, R + (int64_t)jb + (int64_t)jb * ldr, ldr, b));
     TRY(P->L.gemm_acc_tri(P->Y, jb, P->U1, b, R + (int64_t)jb * ldr, ldr, jb, b));
@@ -719,7 +697,6 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
   tsqr_plan_s* p = new (std::nothrow) tsqr_plan_s();
   if (!p) return TSQR_ERR_INVALID_ARG;
   p->m = m_local; p->n = n; p->b = panel_b; p->k = n / panel_b; p->algo = algo;
-  p->fuse = (panel_b == 64);
   p->comm = comm; p->nranks = nranks; p->rank = rank; p->stream = stream;
   Carve c;
   c.base = reinterpret_cast<char*>(workspace);

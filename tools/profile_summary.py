@@ -90,7 +90,9 @@ for fn in sorted(os.listdir(src)):
                     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
                     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
                     "launch__grid_size", "launch__block_size"]
-            heads[k] = [{w: f"{r[h.index(w)]} {u[h.index(w)]}" for w in want if w in h} for r in rr[2:]]
+            nm = h.index("Kernel Name") if "Kernel Name" in h else None
+            heads[k] = [dict({"kernel": r[nm] if nm is not None else ""},
+                             **{w: f"{r[h.index(w)]} {u[h.index(w)]}" for w in want if w in h}) for r in rr[2:]]
 json.dump(heads, open(os.path.join(dst, "ncu_full_headlines.json"), "w"), indent=1)
 print(json.dumps(summary["classes"], indent=1))
 print(json.dumps(heads, indent=1)[:3000])
