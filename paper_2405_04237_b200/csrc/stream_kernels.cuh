@@ -388,6 +388,23 @@ struct UppArgs {
   const int* status;
 };
 
+// optional per-phase cycle counters (build with -DTSQR_UPP_PROF; tools only): waits for the X
+// slot / k halves, DMMA phases, epilogue, TMA-store read wait -- printed for two CTAs
+#ifdef TSQR_UPP_PROF
+#define UPP_PROF_DECL long long pf_[5] = {0, 0, 0, 0, 0}, pf_t_ = 0; const long long pf_s_ = clock64();
+#define UPP_PROF_T0 pf_t_ = clock64();
+#define UPP_PROF_ADD(i) { const long long n_ = clock64(); pf_[i] += n_ - pf_t_; pf_t_ = n_; }
+#define UPP_PROF_PRINT                                                                                  \
+  if (lane == 0 && (blockIdx.x == 0 || blockIdx.x == 77) && (wg == 0 || wg == 5))                      \
+    printf("upp cta %d grp %d wg %d: waitX %lld waitLS %lld mma %lld epi %lld wread %lld total %lld\n", \
+           blockIdx.x, grp, wg, pf_[0], pf_[1], pf_[2], pf_[3], pf_[4], clock64() - pf_s_);
+#else
+#define UPP_PROF_DECL
+#define UPP_PROF_T0
+#define UPP_PROF_ADD(i)
+#define UPP_PROF_PRINT
+#endif
+
 __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant__ UppArgs a) {
   extern __shared__ __align__(128) double smem_raw[];
   if (failed(a.status)) return;
@@ -450,6 +467,7 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
   const int wg = warp % UPP_GW, wr = wg / (UPP_GW / 2), wc = wg % (UPP_GW / 2);
   const int gid = lane >> 2, tig = lane & 3;
   const int c0 = wc * 8 * UPP_NJ;  // first column of this warp's tile within the chunk
+  UPP_PROF_DECL
   int vLS = 0;
   for (int ch = 0; ch < nch; ++ch) {
     const int tl = grp + 2 * (ch / nxc), xc = ch % nxc;
@@ -461,7 +479,9 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
       for (int j = 0; j < UPP_NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int h = 0; h < nkh; ++h, ++vLS) {
       const int sl = vLS & 1;
+      UPP_PROF_T0
       mbar_wait(&fullLS[sl], (vLS >> 1) & 1);
+      UPP_PROF_ADD(1)
       const double* sL = ringL + sl * UPP_LSL + tig * LDT + wr * 32 + gid;
       const double* sS = ringS + sl * UPP_SSL + (c0 + gid) * UPP_LDS + tig;
       // fragments double-buffered in registers: step s+1 is loaded while step s issues
@@ -486,11 +506,14 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&emptyLS[sl]);
+      UPP_PROF_ADD(2)
     }
     // epilogue: X <- X - acc in the slot (all loads before any store: a store may alias a
     // later load for the compiler, and interleaving them serialises the load->add->store
     // chains), then TMA stores of 16 rows x 8*NJ columns per warp
+    UPP_PROF_T0
     mbar_wait(fullX, ch & 1);
+    UPP_PROF_ADD(0)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -517,10 +540,14 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
       }
       bulk_commit();
     }
+    UPP_PROF_ADD(3)
     if (lane == 0) bulk_wait_read0();  // the TMA stores have read the slot
+    __syncwarp();
+    UPP_PROF_ADD(4)
     __syncwarp();
     if (lane == 0) mbar_arrive(emptyX);
   }
+  UPP_PROF_PRINT
   if (lane == 0) bulk_wait0();
 }
 
