@@ -19,8 +19,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CQR2, CQR2GS, MCQR2GS, CQR, CQRGS = 0, 1, 2, 3, 4
-ALGOS = {"cqr2": CQR2, "cqr2gs": CQR2GS, "mcqr2gs": MCQR2GS, "cqr": CQR, "cqrgs": CQRGS}
+CQR2, CQR2GS, MCQR2GS, CQR, CQRGS, SCQR3, SCQR = 0, 1, 2, 3, 4, 5, 6
+ALGOS = {"cqr2": CQR2, "cqr2gs": CQR2GS, "mcqr2gs": MCQR2GS, "cqr": CQR, "cqrgs": CQRGS, "scqr3": SCQR3,
+         "scqr": SCQR}
 OK, ERR_ARG, ERR_BREAKDOWN, ERR_NOMEM = 0, 1, 5, 6
 
 BUILD_CMD = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",

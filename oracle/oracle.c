@@ -46,6 +46,11 @@
 #define ORC_MCQR2GS 2
 #define ORC_CQR 3
 #define ORC_CQRGS 4
+#define ORC_SCQR3 5
+#define ORC_SCQR 6
+
+/* unit roundoff of FP64 round-to-nearest-even: u = 2^-53 */
+#define ORC_UNIT_ROUNDOFF 1.1102230246251565e-16
 
 typedef struct {
   int32_t status;      /* ORC_OK or ORC_ERR_* */
@@ -315,6 +320,35 @@ static int cqr(double* X, int64_t ldx, int64_t m, int64_t b, double* U, int64_t 
   return rc;
 }
 
+/* sCQR(X) -- shifted CholeskyQR (Alg. 4):
+ *   G = X^T X                                   (l.1; row sums of R-3)
+ *   s = sqrt(m) u ||X||_F^2                     (l.2, "calculate shift"; the conservative
+ *                                                Frobenius-norm shift; u = 2^-53)
+ *   W = G + s I                                 (l.3)
+ *   W = U^T U;  X <- X U^{-1}                   (l.4-5)
+ * ||X||_F^2 = sum_j sum_rows x_rj^2 ("summing over the squares of the elements"):
+ * the inner row sums are exactly the Gram diagonal G_jj (same products, same R-3 order), so
+ * ||X||_F^2 = sum_j G_jj, summed over j in index order.  m is the global row count (on
+ * one address space: the rows of X). */
+static int scqr(double* X, int64_t ldx, int64_t m, int64_t b, double* U, int64_t ldu, orc_info* info,
+                double unit_roundoff) {
+  double* W = (double*)malloc(sizeof(double) * (size_t)(b * b));
+  if (!W) return ORC_ERR_NOMEM;
+  int rc = orc_gram(X, ldx, m, b, W, b);
+  if (rc == ORC_OK) {
+    double fro2 = 0.0;
+    for (int64_t j = 0; j < b; ++j) fro2 += W[j + j * b];
+    const double s = sqrt((double)m) * unit_roundoff * fro2;
+    for (int64_t j = 0; j < b; ++j) W[j + j * b] += s;
+    int32_t piv = -1; double pv = 0.0;
+    rc = orc_chol(W, b, b, U, ldu, &piv, &pv);
+    if (rc == ORC_ERR_BREAKDOWN && info) { info->pivot = piv; info->pivot_value = pv; }
+  }
+  if (rc == ORC_OK) orc_rsolve(X, ldx, m, b, U, ldu);
+  free(W);
+  return rc;
+}
+
 static void zero_mat(double* R, int64_t ldr, int64_t p, int64_t q) {
   for (int64_t j = 0; j < q; ++j)
     for (int64_t i = 0; i < p; ++i) R[i + j * ldr] = 0.0;
@@ -450,6 +484,28 @@ int orc_factor(double* A, int64_t lda, int64_t m, int64_t n, int64_t b, int algo
     case ORC_MCQR2GS:
       rc = mcqr2gs(A, lda, m, n, b, R, ldr, info);
       break;
+    case ORC_SCQR: {
+      rc = scqr(A, lda, m, n, R, ldr, info, ORC_UNIT_ROUNDOFF);
+      if (rc != ORC_OK) rc = fail(info, rc, 1, 1, 1);
+      break;
+    }
+    case ORC_SCQR3: {
+      /* sCQR3 (Alg. 5): [Q1, R1] = sCQR(A); [Q, R2] = CQR2(Q1); R = R2 R1.
+       * Breakdown stages: 1 = the shifted CQR, 2 and 3 = the two CQRs of CQR2. */
+      double* R1 = (double*)calloc((size_t)(n * n), sizeof(double));
+      double* R2 = (double*)calloc((size_t)(n * n), sizeof(double));
+      if (!R1 || !R2) { free(R1); free(R2); return fail(info, ORC_ERR_NOMEM, 0, 0, 0); }
+      rc = scqr(A, lda, m, n, R1, n, info, ORC_UNIT_ROUNDOFF);
+      if (rc != ORC_OK) {
+        rc = fail(info, rc, 1, 1, 1);
+      } else {
+        rc = cqr2_block(A, lda, m, n, R2, n, 1, 1, info);
+        if (rc == ORC_ERR_BREAKDOWN && info) info->stage += 1;
+      }
+      if (rc == ORC_OK) orc_matmul(R2, n, R1, n, n, n, n, R, ldr, 1, 0);
+      free(R1); free(R2);
+      break;
+    }
     default:
       return fail(info, ORC_ERR_ARG, 0, 0, 0);
   }

@@ -365,3 +365,65 @@ def test_interlacing_panel_condition(orc):
             c = np.linalg.cond(A[:, :b])
             lower = sigma[n - b] / sigma[b - 1]
             assert c <= kappa * 1.05 + 1e-9 and c * 1.05 >= lower
+
+
+# ---------------------------------------------------------------- shifted CholeskyQR3
+def test_scqr3_matches_householder_small(orc):
+    """Uniqueness of the thin QR: on well-conditioned inputs sCQR3's R equals the
+    sign-normalised Householder R (LAPACK-free here: the oracle's own Householder is pinned
+    against numpy above)."""
+    rng = np.random.default_rng(21)
+    for t in range(20):
+        m, n = int(rng.integers(60, 300)), int(rng.integers(2, 24))
+        A, _, _ = synth.generate_np(m, n, 10.0 ** rng.uniform(0, 4), seed=300 + t, chunk=m)
+        _, Rh = orc.householder(A)
+        Q, R, info = orc.factor(A, n, "scqr3")
+        assert info["status"] == 0
+        assert np.max(np.abs(R - Rh)) <= 1e-10 * np.linalg.norm(A)
+        assert orc.residual(A, Q, R) <= 1e-13
+
+
+@pytest.mark.parametrize("kappa", [1e8, 1e12, 1e15])
+def test_paper_claim_scqr3_ill_conditioned(orc, kappa):
+    """P:254-256 and Fig. orthoscqr3: with the conservative Frobenius shift sCQR3
+    completes through kappa = 1e15 with O(u) orthogonality and residual, where CQR2 (no
+    shift) fails beyond 1e8."""
+    A, _, _ = synth.generate_np(3000, 300, kappa, seed=0, chunk=3000)
+    Q, R, info = orc.factor(A, 300, "scqr3")
+    assert info["status"] == 0
+    assert orc.orthogonality(Q) / math.sqrt(300) <= 1e-13
+    assert orc.residual(A, Q, R) <= 1e-13
+
+
+def test_scqr_shift_makes_singular_gram_factorable(orc):
+    """The shift is what makes the Cholesky succeed (Alg. 4 l.2-3): with an exactly
+    repeated column the unshifted Gram is singular and CQR breaks down, sCQR does not, and
+    its first diagonal entry obeys u_11^2 = g_11 + s with 0 < s << g_11."""
+    A, _, _ = synth.generate_np(2048, 16, 1e3, seed=13)
+    A = np.asfortranarray(np.hstack([A, A[:, :1]]))
+    _, _, info = orc.factor(A, 17, "cqr")
+    assert info["status"] == 5
+    Q, R, info = orc.factor(A, 17, "scqr")
+    assert info["status"] == 0
+    g11 = float(np.dot(A[:, 0], A[:, 0]))
+    s = R[0, 0] ** 2 - g11
+    assert 0.0 < s < 1e-10 * g11
+
+
+def test_scqr3_power_of_two_scaling_bitwise(orc):
+    """Metamorphic pin: s scales with ||A||_F^2, so scaling A by 2^e scales every Gram, shift
+    and Cholesky factor exactly: Q(2^e A) = Q(A) and R(2^e A) = 2^e R(A) bitwise."""
+    A, _, _ = synth.generate_np(4096, 64, 1e14, seed=14)
+    Q, R, i1 = orc.factor(A, 64, "scqr3")
+    Qs, Rs, i2 = orc.factor(np.asfortranarray(np.ldexp(A, 5)), 64, "scqr3")
+    assert i1["status"] == 0 and i2["status"] == 0
+    assert np.array_equal(Q, Qs) and np.array_equal(np.ldexp(R, 5), Rs)
+
+
+def test_scqr3_allreduce_count(orc):
+    """Three Gram reductions (sCQR + CQR2, Alg. 5; "communication 50% higher than CQR2",
+    P:264)."""
+    A, _, _ = synth.generate_np(4096, 32, 1e6, seed=15)
+    orc.reset_reduction_count()
+    _, _, info = orc.factor(A, 32, "scqr3")
+    assert info["status"] == 0 and orc.reduction_count() == 3
