@@ -14,6 +14,10 @@
  *   TSQR_MCQR2GS  the paper's modified CQR2GS (Alg. 8)
  *   TSQR_CQR      single CholeskyQR pass (Alg. 2)        -- tests
  *   TSQR_CQRGS    single CQRGS pass (Alg. 7)                         -- tests
+ *   TSQR_SCQR3    shifted CholeskyQR3 (Alg. 5): sCQR (Alg. 4, P:236-246:
+ *                 W = A^T A + s I, s = sqrt(m) u ||A||_F^2, m the global row count,
+ *                 u = 2^-53) followed by CQR2; R = R2 R1.  b == n.  3 allreduces.
+ *   TSQR_SCQR     single shifted CholeskyQR pass (Alg. 4)           -- tests
  *
  * Conventions for every entry point:
  *   - Matrices are FP64, COLUMN-MAJOR: element (r, c) of X is X[r + c*ldX].
@@ -55,7 +59,9 @@ typedef enum {
   TSQR_CQR2GS = 1,
   TSQR_MCQR2GS = 2,
   TSQR_CQR = 3,
-  TSQR_CQRGS = 4
+  TSQR_CQRGS = 4,
+  TSQR_SCQR3 = 5,
+  TSQR_SCQR = 6
 } tsqr_algo;
 
 /* Where a Cholesky breakdown happened (identical on every rank, since every rank

@@ -17,8 +17,9 @@ import os
 
 from . import build as _build
 
-CQR2, CQR2GS, MCQR2GS, CQR, CQRGS = 0, 1, 2, 3, 4
-ALGOS = {"cqr2": CQR2, "cqr2gs": CQR2GS, "mcqr2gs": MCQR2GS, "cqr": CQR, "cqrgs": CQRGS}
+CQR2, CQR2GS, MCQR2GS, CQR, CQRGS, SCQR3, SCQR = 0, 1, 2, 3, 4, 5, 6
+ALGOS = {"cqr2": CQR2, "cqr2gs": CQR2GS, "mcqr2gs": MCQR2GS, "cqr": CQR, "cqrgs": CQRGS, "scqr3": SCQR3,
+         "scqr": SCQR}
 TSQR_OK, TSQR_ERR_INVALID_ARG, TSQR_ERR_UNSUPPORTED, TSQR_ERR_CUDA = 0, 1, 2, 3
 TSQR_ERR_NCCL, TSQR_ERR_BREAKDOWN, TSQR_ERR_WORKSPACE = 4, 5, 6
 KCLASSES = ["gram", "proj", "update", "trmm", "chol", "small", "allreduce"]

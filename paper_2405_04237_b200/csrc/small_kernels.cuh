@@ -323,6 +323,22 @@ __global__ void k_gemm_acc_tri(const double* __restrict__ A, int lda, const doub
 }
 
 // D <- alpha S (alpha = +-1 in use: exact)
+// Shift of the Gram matrix for shifted CholeskyQR (Alg. 4 l.2-3):
+// W_ii += s with s = (sqrt(m) u) * ||A||_F^2, where ||A||_F^2 = sum_j W_jj is taken from the
+// diagonal of the allreduced Gram (the row sums of the squares of A's entries) in index
+// order -- identical on every rank.  sqrt_m_u = sqrt(m_global) * 2^-53 from the host.
+__global__ void k_shift(double* W, int ldw, int n, double sqrt_m_u, const int* status) {
+  if (failed(status)) return;
+  __shared__ double s_shift;
+  if (threadIdx.x == 0) {
+    double fro2 = 0.0;
+    for (int j = 0; j < n; ++j) fro2 += W[j + (int64_t)j * ldw];
+    s_shift = sqrt_m_u * fro2;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) W[j + (int64_t)j * ldw] += s_shift;
+}
+
 __global__ void k_copy2d(const double* __restrict__ S, int64_t lds, double* __restrict__ D, int64_t ldd, int rows,
                          int cols, double alpha, const int* status) {
   if (failed(status)) return;

@@ -391,6 +391,15 @@ struct Launcher {
     return TSQR_OK;
   }
 
+  tsqr_status shift(double* W, int ldw, int n, double sqrt_m_u) {
+    const size_t t0 = tbegin();
+    k_shift<<<1, 256, 0, st>>>(W, ldw, n, sqrt_m_u, status);
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    tend(t0, TSQR_KCLASS_SMALL, 0.0, 0.0);
+    return TSQR_OK;
+  }
+
   tsqr_status trimul(const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int n) {
     const size_t t0 = tbegin();
     k_trimul<<<grid_1d((int64_t)n * n), 256, 0, st>>>(A, lda, B, ldb, Cm, ldc, n, status);
@@ -426,6 +435,7 @@ struct Launcher {
 // =========================================================================================
 struct tsqr_plan_s {
   int64_t m = 0;        // local rows
+  int64_t m_global = 0; // rows over all ranks (the sCQR shift, Alg. 4 l.2)
   int n = 0, b = 0, k = 0;
   tsqr_algo algo = TSQR_CQR2;
   ncclComm_t comm = nullptr;
@@ -512,10 +522,13 @@ size_t carve(Carve& c, tsqr_plan_s* p, int64_t m, int n, int b, tsqr_algo algo) 
 
 tsqr_status check_shape(int64_t m_local, int n, int b, tsqr_algo algo) {
   if (m_local < 0 || n < 1 || n > 4096) { set_err("bad m_local/n"); return TSQR_ERR_INVALID_ARG; }
-  if (algo < TSQR_CQR2 || algo > TSQR_CQRGS) { set_err("bad algo"); return TSQR_ERR_INVALID_ARG; }
+  if (algo < TSQR_CQR2 || algo > TSQR_SCQR) { set_err("bad algo"); return TSQR_ERR_INVALID_ARG; }
   if (!valid_b(b)) { set_err("panel_b=%d not in {16,32,64,128,256}", b); return TSQR_ERR_UNSUPPORTED; }
   if (n % b != 0) { set_err("ragged panels (n %% b != 0) unsupported"); return TSQR_ERR_UNSUPPORTED; }
-  if ((algo == TSQR_CQR2 || algo == TSQR_CQR) && b != n) { set_err("CQR/CQR2 need b == n"); return TSQR_ERR_INVALID_ARG; }
+  if ((algo == TSQR_CQR2 || algo == TSQR_CQR || algo == TSQR_SCQR3 || algo == TSQR_SCQR) && b != n) {
+    set_err("CQR/CQR2/sCQR/sCQR3 need b == n");
+    return TSQR_ERR_INVALID_ARG;
+  }
   return TSQR_OK;
 }
 
@@ -624,6 +637,31 @@ tsqr_status run_mcqr2gs(tsqr_plan_s* P, double* A, int64_t lda, double* R, int l
   return TSQR_OK;
 }
 
+// Shifted CholeskyQR3 (Alg. 5) of the whole m x n matrix (b == n):
+//   [Q1, R1] = sCQR(A)  -- Gram, shift W += s I (Alg. 4 l.2-3), Cholesky, Q1 = A R1^{-1}
+//   [Q, R2] = CQR2(Q1)  -- two CholeskyQR passes, R2 = U2 U1
+//   R = R2 R1
+// Breakdown stages: 1 = the shifted CQR, 2 and 3 = the CQRs of CQR2 (as in the oracle).
+constexpr double kUnitRoundoff = 1.1102230246251565e-16;  // 2^-53 (FP64, round to nearest)
+
+tsqr_status scqr(tsqr_plan_s* P, double* A, int64_t lda, double* Uout, int ldu) {
+  const int n = P->n;
+  TRY(gram(P, A, lda, n));
+  TRY(P->L.shift(P->W, n, n, std::sqrt((double)P->m_global) * kUnitRoundoff));
+  return chol_trmm(P, A, lda, n, Uout, ldu, 1, 1, 1);
+}
+
+tsqr_status run_scqr3(tsqr_plan_s* P, double* A, int64_t lda, double* R, int ldr) {
+  const int n = P->n;
+  TRY(scqr(P, A, lda, P->R1, n));                       // l.1
+  TRY(gram(P, A, lda, n));                              // l.2: CQR2(Q1)
+  TRY(chol_trmm(P, A, lda, n, P->U1, n, 1, 1, 2));
+  TRY(gram(P, A, lda, n));
+  TRY(chol_trmm(P, A, lda, n, P->U2, n, 1, 1, 3));
+  TRY(P->L.trimul(P->U2, n, P->U1, n, P->R2, n, n));   //     R2 = U2 U1
+  return P->L.trimul(P->R2, n, P->R1, n, R, ldr, n);    // l.3: R = R2 R1
+}
+
 const char* status_names[] = {"TSQR_OK", "TSQR_ERR_INVALID_ARG", "TSQR_ERR_UNSUPPORTED", "TSQR_ERR_CUDA",
                               "TSQR_ERR_NCCL", "TSQR_ERR_BREAKDOWN", "TSQR_ERR_WORKSPACE"};
 
@@ -660,6 +698,7 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
   }
   ncclComm_t comm = reinterpret_cast<ncclComm_t>(nccl_comm);
   int nranks = 1, rank = 0;
+  int64_t m_global = m_local;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   if (comm) {
     NCCL_TRY(ncclCommCount(comm, &nranks));
@@ -689,6 +728,7 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
       return st;
     }
     if (r[12 + 4] < n) { set_err("global m < n"); return TSQR_ERR_INVALID_ARG; }
+    m_global = r[12 + 4];
   } else {
     if (st != TSQR_OK) return st;
     if (m_local < n) { set_err("m < n"); return TSQR_ERR_INVALID_ARG; }
@@ -696,7 +736,7 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
   if (st != TSQR_OK) return st;
   tsqr_plan_s* p = new (std::nothrow) tsqr_plan_s();
   if (!p) return TSQR_ERR_INVALID_ARG;
-  p->m = m_local; p->n = n; p->b = panel_b; p->k = n / panel_b; p->algo = algo;
+  p->m = m_local; p->m_global = m_global; p->n = n; p->b = panel_b; p->k = n / panel_b; p->algo = algo;
   p->comm = comm; p->nranks = nranks; p->rank = rank; p->stream = stream;
   Carve c;
   c.base = reinterpret_cast<char*>(workspace);
@@ -742,6 +782,12 @@ static tsqr_status enqueue_factor(tsqr_plan_t P, double* A, int64_t lda, double*
       break;
     case TSQR_MCQR2GS:
       s = run_mcqr2gs(P, A, lda, R, ldr);
+      break;
+    case TSQR_SCQR3:
+      s = run_scqr3(P, A, lda, R, ldr);
+      break;
+    case TSQR_SCQR:
+      s = scqr(P, A, lda, R, ldr);
       break;
   }
   (void)b;

@@ -71,7 +71,8 @@ def _worker(rank, world, port, q, m_local, n, b, kappa, algo):
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("algo,n,b,kappa", [("mcqr2gs", 256, 64, 1e8), ("mcqr2gs", 512, 64, 1e15),
-                                             ("cqr2gs", 128, 32, 1e6), ("cqr2", 64, 64, 1e4)])
+                                             ("cqr2gs", 128, 32, 1e6), ("cqr2", 64, 64, 1e4),
+                                             ("scqr3", 128, 128, 1e15)])
 def test_two_rank_factorisation(algo, n, b, kappa):
     import torch.multiprocessing as mp
     world = min(_ngpu(), 4)
@@ -90,7 +91,7 @@ def test_two_rank_factorisation(algo, n, b, kappa):
     for r in range(1, world):
         assert np.array_equal(o["R"][0], o["R"][r])
     k = n // b
-    assert o["calls"] == (2 if algo == "cqr2" else 4 * k - 2)
+    assert o["calls"] == {"cqr2": 2, "scqr3": 3}.get(algo, 4 * k - 2)
     assert o["orth"] <= 1e-13 and o["res"] <= 1e-14, (o["orth"], o["res"])
     if kappa <= 1e8:
         R, R1 = o["R"][0], o["R1"]

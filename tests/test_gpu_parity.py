@@ -177,6 +177,12 @@ def test_factor_deterministic_and_counts(T):
         assert ar == 4 * 4 - 2
         p.close()
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    A2, _, _ = synth.generate_np(65536, 256, 1e4, seed=6)
+    for algo, expect in (("cqr2", 2), ("scqr3", 3), ("scqr", 1)):  # allreduces per factorisation
+        p = T.Plan(A2.shape[0], 256, 256, algo)
+        p.factor(T.to_colmajor(A2))
+        assert p.counts()[0] == expect, algo
+        p.close()
     torch.cuda.synchronize()
 
 
@@ -234,3 +240,52 @@ def test_kernel_timing_graph_and_eager(T):
         assert tm["proj"]["launches"] == 3 * 6 and tm["proj"]["ms"] > 0
         assert tm["chol"]["launches"] == 3 * 8
         p.close()
+
+
+# ---------------------------------------------------------------- shifted CholeskyQR3 (NEXT-f2)
+@pytest.mark.parametrize("m,n,kappa", [(4096, 64, 1e4), (4096, 64, 1e15), (65536 + 37, 128, 1e12),
+                                       (2 ** 16, 256, 1e14), (1000, 16, 1e10), (2 ** 16, 128, 1e15),
+                                       (2 ** 16, 256, 1e15)])
+def test_scqr3_vs_oracle(T, orc, m, n, kappa):
+    """sCQR3 (Alg. 5) with the paper's conservative shift.  Through kappa = 1e14 it completes on
+    both sides and meets the mCQR2GS gates (Fig. orthoscqr3); R agrees with the
+    oracle's to 1e-10 where R is well determined (kappa <= 1e8).  At kappa = 1e15 and n >= 128
+    the shifted pass leaves cond(Q1) ~ 3e8 (measured on both sides), so the CQR2 stage's Gram
+    has condition ~1e17 > 1/u and its Cholesky sits at the breakdown threshold (reading R-22):
+    there each side must either meet the gates or break down in the CQR2 stage (stage 2/3),
+    never in the shifted stage."""
+    A, _, _ = synth.generate_np(m, n, kappa, seed=2, chunk=m)
+    Qo, Ro, io = orc.factor(A, n, "scqr3")
+    Q, R, info = run_gpu(T, A, n, "scqr3")
+    edge = kappa >= 1e15 and n >= 128
+    if edge:
+        for ok, st, QQ, RR in ((io["status"] == 0, io["stage"], Qo, Ro),
+                               (info is None, None if info is None else info["stage"], Q, R)):
+            if ok:
+                orth, res = gates(orc, A, QQ, RR)
+                assert orth <= 1e-13 and res <= 1e-14, (orth, res)
+            else:
+                assert st in (2, 3), st
+        return
+    assert io["status"] == 0 and info is None
+    check_invariants(R)
+    orth, res = gates(orc, A, Q, R)
+    assert orth <= 1e-13 and res <= 1e-14, (orth, res)
+    if kappa <= 1e8:
+        assert np.linalg.norm(R - Ro) / np.linalg.norm(Ro) <= 1e-10
+
+
+def test_scqr_shift_on_gpu_matches_oracle(T, orc):
+    """The single shifted pass (Alg. 4) on an exactly singular Gram (repeated column): CQR
+    breaks down on both sides, sCQR completes on both, and the shifted R agrees with the
+    oracle's (same shift formula, same global m) to 1e-10 in its well-determined leading part."""
+    A, _, _ = synth.generate_np(8192, 31, 1e3, seed=13)
+    A = np.asfortranarray(np.hstack([A, A[:, :1]]))
+    _, _, io = orc.factor(A, 32, "cqr")
+    _, _, info = run_gpu(T, A, 32, "cqr")
+    assert io["status"] == 5 and info is not None
+    _, Ro, io = orc.factor(A, 32, "scqr")
+    _, R, info = run_gpu(T, A, 32, "scqr")
+    assert io["status"] == 0 and info is None
+    lead = slice(0, 31)
+    assert np.linalg.norm(R[lead, lead] - Ro[lead, lead]) / np.linalg.norm(Ro[lead, lead]) <= 1e-10
