@@ -13,8 +13,8 @@ namespace tsqr {
 // -----------------------------------------------------------------------------------------
 // One CTA of 8 warps per 32 consecutive elements: warp w sums the partials s = w (mod 8) with
 // 4 interleaved running sums, then lane l of warp 0 adds the 8 warp sums pairwise -- a fixed
-// order (deterministic) with 8x the memory parallelism of one thread per element (the fused
-// Gram reductions have 2 x 148 partials).
+// order (deterministic) with 8x the memory parallelism of one thread per element (split counts
+// reach ~150-300 partials per output).
 constexpr int RED_NT = 256;
 __global__ void __launch_bounds__(RED_NT) k_reduce(const double* __restrict__ part, int Sfull, int Sdiag, int p,
                                                    int q, int ldp, int64_t pstride, double* __restrict__ out,
