@@ -127,9 +127,14 @@ tsqr_status tsqr_last_counts(tsqr_plan_t plan, int64_t* allreduces, int64_t* lau
 /* Factor from HOST buffers (the end-to-end form of tsqr_factor): A_host (m_local x n,
  * ld lda_host) is copied to the caller's device buffer A_dev (ld lda_dev), factored in
  * place, and Q is copied back over A_host; R is produced in R_dev (device, ldr_dev) and
- * copied to R_host (ld ldr_host).  All copies are cudaMemcpy2DAsync on the plan's stream
- * (asynchronous only if the host buffers are pinned, e.g. cudaHostAlloc / torch
- * pin_memory).  COLLECTIVE like tsqr_factor; completes at tsqr_wait. */
+ * copied to R_host (ld ldr_host).  The host->device copy runs on the plan's stream before
+ * the factorisation (every column is read by the first projection); for the panel-wise
+ * methods (MCQR2GS, CQR2GS with k > 1) each panel Q_j is copied back on a plan-owned
+ * second stream as soon as it is final, overlapping the remaining panels; otherwise Q is
+ * copied back after the factorisation.  Copies are cudaMemcpy2DAsync (asynchronous only
+ * if the host buffers are pinned, e.g. cudaHostAlloc / torch pin_memory); A_host must
+ * not be touched until tsqr_wait returns.  COLLECTIVE like tsqr_factor; completes at
+ * tsqr_wait (which orders the plan stream after the copies). */
 tsqr_status tsqr_factor_host(tsqr_plan_t plan, double* A_host, int64_t lda_host, double* R_host,
                              int32_t ldr_host, double* A_dev, int64_t lda_dev, double* R_dev,
                              int32_t ldr_dev);

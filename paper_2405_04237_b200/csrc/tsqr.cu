@@ -466,7 +466,17 @@ struct tsqr_plan_s {
   int64_t glda = 0;
   int32_t gldr = 0;
   bool gtiming = false;
+  // tsqr_factor_host: per-panel "Q_j is final" events (recorded inside the graph as external
+  // event nodes while capturing) so the device->host copy of Q_j overlaps the later panels
+  bool panel_events = false, gpanel = false;
+  std::vector<cudaEvent_t> ev_panel;
+  cudaStream_t d2h = nullptr;
+  cudaEvent_t ev_d2h = nullptr, ev_fact = nullptr;
   ~tsqr_plan_s() {
+    for (cudaEvent_t e : ev_panel) cudaEventDestroy(e);
+    if (ev_d2h) cudaEventDestroy(ev_d2h);
+    if (ev_fact) cudaEventDestroy(ev_fact);
+    if (d2h) cudaStreamDestroy(d2h);
     if (exec) cudaGraphExecDestroy(exec);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
@@ -545,6 +555,13 @@ tsqr_status allreduce(tsqr_plan_s* P, double* buf, size_t count) {
   return TSQR_OK;
 }
 
+// panel j's columns of Q are final (no later step writes them): signal tsqr_factor_host
+tsqr_status panel_done(tsqr_plan_s* P, int j) {
+  if (!P->panel_events || j >= (int)P->ev_panel.size()) return TSQR_OK;
+  CUDA_TRY(cudaEventRecordWithFlags(P->ev_panel[j], P->L.st, P->timer.capturing ? cudaEventRecordExternal : 0u));
+  return TSQR_OK;
+}
+
 // W <- allreduce(X^T X), X = m x w slab (standalone split-row Gram)
 tsqr_status gram(tsqr_plan_s* P, const double* X, int64_t ldx, int w) {
   TRY(P->L.atb(X, ldx, X, ldx, P->m, w, w, true, P->part, P->W, w));
@@ -598,6 +615,7 @@ tsqr_status cqrgs_pass(tsqr_plan_s* P, double* A, int64_t lda, double* Rp, int l
     TRY(gram(P, Aj, lda, b));                                                  // l.2-3
     // l.4-6: R_jj = U (the Cholesky writes straight into R's diagonal block)
     TRY(chol_trmm(P, Aj, lda, b, Rp + (int64_t)j * b + (int64_t)j * b * ldr, ldr, pass, j + 1, 1));
+    if (pass == 2) TRY(panel_done(P, j));
     const int nt = n - (j + 1) * b;
     if (nt > 0) {
       double* At = A + (int64_t)(j + 1) * b * lda;
@@ -612,6 +630,7 @@ tsqr_status cqrgs_pass(tsqr_plan_s* P, double* A, int64_t lda, double* Rp, int l
 tsqr_status run_mcqr2gs(tsqr_plan_s* P, double* A, int64_t lda, double* R, int ldr) {
   const int n = P->n, b = P->b, k = P->k;
   TRY(cqr2_block(P, A, lda, b, R, ldr));                                      // l.1
+  TRY(panel_done(P, 0));
   for (int j = 1; j < k; ++j) {
     double* Ap = A + (int64_t)(j - 1) * b * lda;  // Q_{j-1}
     double* Aj = A + (int64_t)j * b * lda;
@@ -630,6 +649,7 @@ tsqr_status run_mcqr2gs(tsqr_plan_s* P, double* A, int64_t lda, double* R, int l
     // l.8: second CQR -> Q_j, U2
     TRY(gram(P, Aj, lda, b));
     TRY(chol_trmm(P, Aj, lda, b, P->U2, b, 1, j + 1, 2));
+    TRY(panel_done(P, j));
     // R_jj = U2 U1; R_{1:j-1,j} += C U1  (R-8)
     TRY(P->L.trimul(P->U2, b, P->U1, b, R + (int64_t)jb + (int64_t)jb * ldr, ldr, b));
     TRY(P->L.gemm_acc_tri(P->Y, jb, P->U1, b, R + (int64_t)jb * ldr, ldr, jb, b));
@@ -820,7 +840,7 @@ tsqr_status tsqr_factor(tsqr_plan_t P, double* A, int64_t lda, double* R, int32_
   CUDA_TRY(cudaEventRecord(P->ev_in, P->stream));
   CUDA_TRY(cudaStreamWaitEvent(P->gstream, P->ev_in, 0));
   const bool same = P->exec && P->gA == A && P->glda == lda && P->gR == R && P->gldr == ldr &&
-                    P->gtiming == P->timer.on;
+                    P->gtiming == P->timer.on && P->gpanel == P->panel_events;
   if (!same) {
     // capture the whole factorisation (kernels, NCCL allreduces, timing events) once
     if (P->exec) {
@@ -855,7 +875,7 @@ tsqr_status tsqr_factor(tsqr_plan_t P, double* A, int64_t lda, double* R, int32_
       return TSQR_ERR_CUDA;
     }
     P->timer.graph_recs = P->timer.on;
-    P->gA = A; P->glda = lda; P->gR = R; P->gldr = ldr; P->gtiming = P->timer.on;
+    P->gA = A; P->glda = lda; P->gR = R; P->gldr = ldr; P->gtiming = P->timer.on; P->gpanel = P->panel_events;
   }
   CUDA_TRY(cudaGraphLaunch(P->exec, P->gstream));
   CUDA_TRY(cudaEventRecord(P->ev_out, P->gstream));
@@ -916,15 +936,49 @@ tsqr_status tsqr_factor_host(tsqr_plan_t P, double* A_host, int64_t lda_host, do
     return TSQR_ERR_INVALID_ARG;
   }
   const size_t rowb = sizeof(double) * (size_t)P->m;
+  // the panel-wise methods finalise Q one panel at a time: copy Q_j back on a second stream as
+  // soon as it is final, overlapping the remaining panels (H2D has to complete first: the first
+  // projection reads every column)
+  const bool by_panel = P->m > 0 && P->k > 1 && (P->algo == TSQR_MCQR2GS || P->algo == TSQR_CQR2GS);
+  if (!P->d2h) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->d2h, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_d2h, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fact, cudaEventDisableTiming));
+  }
+  if (by_panel && (int)P->ev_panel.size() < P->k) {
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    while ((int)P->ev_panel.size() < P->k) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      P->ev_panel.push_back(e);
+    }
+  }
   if (P->m > 0)
     CUDA_TRY(cudaMemcpy2DAsync(A_dev, sizeof(double) * lda_dev, A_host, sizeof(double) * lda_host, rowb, P->n,
                                cudaMemcpyHostToDevice, P->stream));
-  TRY(tsqr_factor(P, A_dev, lda_dev, R_dev, ldr_dev));
-  if (P->m > 0)
-    CUDA_TRY(cudaMemcpy2DAsync(A_host, sizeof(double) * lda_host, A_dev, sizeof(double) * lda_dev, rowb, P->n,
-                               cudaMemcpyDeviceToHost, P->stream));
+  P->panel_events = by_panel;
+  const tsqr_status fs = tsqr_factor(P, A_dev, lda_dev, R_dev, ldr_dev);
+  P->panel_events = false;
+  TRY(fs);
+  CUDA_TRY(cudaEventRecord(P->ev_fact, P->stream));
+  if (by_panel) {
+    for (int j = 0; j < P->k; ++j) {
+      CUDA_TRY(cudaStreamWaitEvent(P->d2h, P->ev_panel[j], 0));
+      CUDA_TRY(cudaMemcpy2DAsync(A_host + (int64_t)j * P->b * lda_host, sizeof(double) * lda_host,
+                                 A_dev + (int64_t)j * P->b * lda_dev, sizeof(double) * lda_dev, rowb, P->b,
+                                 cudaMemcpyDeviceToHost, P->d2h));
+    }
+    CUDA_TRY(cudaStreamWaitEvent(P->d2h, P->ev_fact, 0));
+  } else {
+    CUDA_TRY(cudaStreamWaitEvent(P->d2h, P->ev_fact, 0));
+    if (P->m > 0)
+      CUDA_TRY(cudaMemcpy2DAsync(A_host, sizeof(double) * lda_host, A_dev, sizeof(double) * lda_dev, rowb, P->n,
+                                 cudaMemcpyDeviceToHost, P->d2h));
+  }
   CUDA_TRY(cudaMemcpy2DAsync(R_host, sizeof(double) * ldr_host, R_dev, sizeof(double) * ldr_dev,
-                             sizeof(double) * P->n, P->n, cudaMemcpyDeviceToHost, P->stream));
+                             sizeof(double) * P->n, P->n, cudaMemcpyDeviceToHost, P->d2h));
+  CUDA_TRY(cudaEventRecord(P->ev_d2h, P->d2h));
+  CUDA_TRY(cudaStreamWaitEvent(P->stream, P->ev_d2h, 0));  // tsqr_wait on the plan stream covers the copies
   return TSQR_OK;
 }
 

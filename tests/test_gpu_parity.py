@@ -289,3 +289,29 @@ def test_scqr_shift_on_gpu_matches_oracle(T, orc):
     assert io["status"] == 0 and info is None
     lead = slice(0, 31)
     assert np.linalg.norm(R[lead, lead] - Ro[lead, lead]) / np.linalg.norm(Ro[lead, lead]) <= 1e-10
+
+
+@pytest.mark.parametrize("algo,b", [("mcqr2gs", 64), ("cqr2gs", 32), ("cqr2", 128), ("scqr3", 128)])
+def test_factor_host_equals_device_factor(T, algo, b):
+    """tsqr_factor_host (pinned host buffers; Q_j copied back panel by panel while the later
+    panels are factored) returns bitwise the Q and R of tsqr_factor on the same input, and
+    the plan can alternate between the two entry points (graph recapture)."""
+    import torch
+    m, n = 65536 + 64, 128
+    A, _, _ = synth.generate_np(m, n, 1e6, seed=21, chunk=m)
+    p = T.Plan(m, n, b, algo)
+    Ad = T.to_colmajor(A)
+    R = p.factor(Ad)
+    Qd, Rd = Ad.cpu().numpy(), R.cpu().numpy()
+    Ah = torch.from_numpy(np.array(A, order="F")).T.contiguous().T.pin_memory()  # column-major host copy
+    Rh = torch.zeros((n, n), dtype=torch.float64).T.contiguous().T.pin_memory()
+    for _ in range(2):
+        Ah.copy_(torch.from_numpy(np.array(A, order="F")))
+        A_dev = T.colmajor_empty(m, n)
+        R_dev = T.colmajor_empty(n, n)
+        p.factor_host(Ah, Rh, A_dev, R_dev)
+        p.wait()
+        assert np.array_equal(Ah.numpy(), Qd) and np.array_equal(Rh.numpy(), Rd)
+    Ad = T.to_colmajor(A)
+    assert np.array_equal(p.factor(Ad).cpu().numpy(), Rd)
+    p.close()
