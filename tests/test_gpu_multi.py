@@ -30,7 +30,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, m_local, n, b, kappa, algo):
+def _worker(rank, world, port, q, m_local, n, b, kappa, algo, cuts=None):
     import sys
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -40,7 +40,7 @@ def _worker(rank, world, port, q, m_local, n, b, kappa, algo):
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        _work(rank, world, q, m_local, n, b, kappa, algo)
+        _work(rank, world, q, m_local, n, b, kappa, algo, cuts)
     except BaseException as e:  # report instead of leaving the parent waiting on the queue
         q.put((rank, {"error": repr(e)}))
         raise
@@ -48,7 +48,7 @@ def _worker(rank, world, port, q, m_local, n, b, kappa, algo):
         dist.destroy_process_group()
 
 
-def _work(rank, world, q, m_local, n, b, kappa, algo):
+def _work(rank, world, q, m_local, n, b, kappa, algo, cuts):
     import torch
     import torch.distributed as dist
     import paper_2405_04237_b200 as t
@@ -56,8 +56,16 @@ def _work(rank, world, q, m_local, n, b, kappa, algo):
     from harness import verify
     comm = t.NcclComm(rank, world, rank)
     m = m_local * world
-    A = t.colmajor_empty(m_local, n, device=f"cuda:{rank}")
-    synth.generate_torch(A, m, rank * m_local, n, kappa, seed=1, chunk=min(m_local, 65536))
+    if cuts is None:  # equal block rows
+        A = t.colmajor_empty(m_local, n, device=f"cuda:{rank}")
+        synth.generate_torch(A, m, rank * m_local, n, kappa, seed=1, chunk=min(m_local, 65536))
+    else:  # uneven block rows [cuts[rank], cuts[rank+1]) of the same global matrix
+        Af = t.colmajor_empty(m, n, device=f"cuda:{rank}")
+        synth.generate_torch(Af, m, 0, n, kappa, seed=1, chunk=min(m_local, 65536))
+        m_local = cuts[rank + 1] - cuts[rank]
+        A = t.colmajor_empty(m_local, n, device=f"cuda:{rank}")
+        A.copy_(Af[cuts[rank]:cuts[rank + 1]])
+        del Af
     A0 = A.clone()
     plan = t.Plan(m_local, n, b, algo, comm=comm, device=f"cuda:{rank}")
     R = plan.factor(A)
@@ -83,13 +91,29 @@ def _work(rank, world, q, m_local, n, b, kappa, algo):
                                              ("cqr2gs", 128, 32, 1e6), ("cqr2", 64, 64, 1e4),
                                              ("scqr3", 128, 128, 1e12)])
 def test_two_rank_factorisation(algo, n, b, kappa):
+    _run_ranks(algo, n, b, kappa)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_uneven_block_rows():
+    """m_local may differ per rank (tsqr_create sums it collectively): ragged, non-multiple-
+    of-64 block rows of the same global matrix give the same R as the single-GPU run."""
+    world = min(_ngpu(), 4)
+    m = world << 17
+    cuts = [0] + [int(m * (r + 1) / world) + (1000 * (r + 1) if r + 1 < world else 0) - 37 * r
+                  for r in range(world - 1)] + [m]
+    _run_ranks("mcqr2gs", 256, 64, 1e6, cuts=cuts)
+
+
+def _run_ranks(algo, n, b, kappa, cuts=None):
     import torch.multiprocessing as mp
     world = min(_ngpu(), 4)
     m_local = 1 << 17
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, m_local, n, b, kappa, algo)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, m_local, n, b, kappa, algo, cuts))
+             for r in range(world)]
     for p in procs:
         p.start()
     outs = {}
