@@ -357,20 +357,29 @@ __global__ void __launch_bounds__(NTHR, 1) k_update(const __grid_constant__ UpdA
 // =========================================================================================
 // k_update_pp: update X -= L S (TMA operands; Alg. 7 l.9 P:351, Alg. 8 l.4 P:465 and l.7
 // P:468) by two independent consumer warp groups.  Each group owns alternate 64-row tiles and
-// walks all 64-column chunks of its tile with its own producer warp, 2-slot ring of 32-wide k
-// halves (L half: [32 cols][68 rows], S half: [64 cols][36 k], both conflict-free for the
-// m8n8k4 fragments) and swizzled X slot (TMA load in, X - acc written back in place, TMA
-// stores out).  With GW = 8 warps per group (32x16 warp tiles) every SMSP hosts two warps of
-// each group, so while one group runs its epilogue the other still has two warps per SMSP
-// issuing DMMAs -- one warp per SMSP cannot keep the DMMA pipe full on shared-memory operands
-// (measured ~30 of 37 TF; strict alternation of two 4-warp groups ran at exactly that rate).
-// Registers are moved from the producer warpgroup to the consumers with setmaxnreg.
+// walks all 64-column chunks of its tile with its own producer warp and 2-slot ring of 32-wide
+// k halves (L half: [32 cols][68 rows], S half: [64 cols][36 k], both conflict-free for the
+// m8n8k4 fragments).  Epilogue (UPP_RED, default): -acc goes into a 128B-swizzled slot and
+// per-warp TMA REDUCE-ADD boxes (cp.reduce.async.bulk.tensor .add, FLOAT64) add it into X in
+// the L2 -- X is never loaded into the SM, and the X - acc subtraction costs no DADD (DADDs
+// queue on the FP64/DMMA pipe behind the other group's DMMAs); the L2's add is the same IEEE
+// operation, so results are bitwise those of the load / subtract / store epilogue
+// (UPP_RED = 0: TMA load of X into the slot, X - acc in place, TMA stores), ~2% slower at cfg3.
+// With GW = 8 warps per group (32x16 warp tiles) every SMSP hosts two warps of each group, so
+// while one group runs its epilogue the other still has two warps per SMSP issuing DMMAs --
+// one warp per SMSP cannot keep the DMMA pipe full on shared-memory operands (measured ~30 of
+// 37 TF; strict alternation of two 4-warp groups ran at exactly that rate).  Registers are
+// moved from the producer warpgroup to the consumers with setmaxnreg.
 // =========================================================================================
 constexpr int UPP_GW = 8;                                  // warps per consumer group
 constexpr int UPP_NJ = 16 / UPP_GW;                        // 8-column blocks per warp tile
 constexpr int UPP_NTHR = (2 * UPP_GW + 4) * 32;            // + one producer warpgroup
 constexpr int UPP_REG_CONS = UPP_GW == 8 ? 104 : 232;      // setmaxnreg budgets
 constexpr int UPP_REG_PROD = 40;
+#ifndef TSQR_UPP_RED
+#define TSQR_UPP_RED 1
+#endif
+constexpr bool UPP_RED = TSQR_UPP_RED;  // epilogue: -acc through the slot + TMA reduce-add into X
 constexpr int UPP_LSL = 32 * LDT;          // L half slot (doubles)
 constexpr int UPP_LDS = 36;                // S half slot leading dimension
 constexpr int UPP_SSL = 64 * UPP_LDS;      // S half slot (doubles)
@@ -456,6 +465,7 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
         tma_load_2d(ringL + sl * UPP_LSL, &a.mapL, (int)row0, h * 32, &fullLS[sl]);
         tma_load_2d(ringS + sl * UPP_SSL, &a.mapS, h * 32, xc * 64, &fullLS[sl]);
       }
+      if (UPP_RED) continue;  // X is never loaded: the L2 adds -acc into it
       if (ch > 0) mbar_wait(emptyX, (ch - 1) & 1);
       mbar_arrive_expect_tx(fullX, XSLOT * 8);
       for (int t = 0; t < 4; ++t) tma_load_2d(sX + t * 1024, &a.mapX, (int)(row0 + 16 * t), xc * 64, fullX);
@@ -511,32 +521,46 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
     // epilogue: X <- X - acc in the slot (all loads before any store: a store may alias a
     // later load for the compiler, and interleaving them serialises the load->add->store
     // chains), then TMA stores of 16 rows x 8*NJ columns per warp
-    UPP_PROF_T0
-    mbar_wait(fullX, ch & 1);
-    UPP_PROF_ADD(0)
+    if (UPP_RED) {  // slot <- -acc (sign flips on the integer pipe; the previous reduce has read it)
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < UPP_NJ; ++j) {
-        const int r = wr * 32 + i * 8 + gid, col = c0 + j * 8 + 2 * tig;
-        acc[i][j][0] = sX[xs_idx(col, r)] - acc[i][j][0];
-        acc[i][j][1] = sX[xs_idx(col + 1, r)] - acc[i][j][1];
-      }
+        for (int j = 0; j < UPP_NJ; ++j) {
+          const int r = wr * 32 + i * 8 + gid, col = c0 + j * 8 + 2 * tig;
+          sX[xs_idx(col, r)] = __longlong_as_double(__double_as_longlong(acc[i][j][0]) ^ (long long)0x8000000000000000ULL);
+          sX[xs_idx(col + 1, r)] = __longlong_as_double(__double_as_longlong(acc[i][j][1]) ^ (long long)0x8000000000000000ULL);
+        }
+    } else {
+      UPP_PROF_T0
+      mbar_wait(fullX, ch & 1);
+      UPP_PROF_ADD(0)
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < UPP_NJ; ++j) {
-        const int r = wr * 32 + i * 8 + gid, col = c0 + j * 8 + 2 * tig;
-        sX[xs_idx(col, r)] = acc[i][j][0];
-        sX[xs_idx(col + 1, r)] = acc[i][j][1];
-      }
+        for (int j = 0; j < UPP_NJ; ++j) {
+          const int r = wr * 32 + i * 8 + gid, col = c0 + j * 8 + 2 * tig;
+          acc[i][j][0] = sX[xs_idx(col, r)] - acc[i][j][0];
+          acc[i][j][1] = sX[xs_idx(col + 1, r)] - acc[i][j][1];
+        }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < UPP_NJ; ++j) {
+          const int r = wr * 32 + i * 8 + gid, col = c0 + j * 8 + 2 * tig;
+          sX[xs_idx(col, r)] = acc[i][j][0];
+          sX[xs_idx(col + 1, r)] = acc[i][j][1];
+        }
+    }
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int box = 2 * wr + t;
-        tma_store_2d(&a.mapXs, (int)(row0 + 16 * box), xc * 64 + c0, sX + box * 1024 + c0 * 16);
+        if (UPP_RED)
+          tma_reduce_add_2d(&a.mapXs, (int)(row0 + 16 * box), xc * 64 + c0, sX + box * 1024 + c0 * 16);
+        else
+          tma_store_2d(&a.mapXs, (int)(row0 + 16 * box), xc * 64 + c0, sX + box * 1024 + c0 * 16);
       }
       bulk_commit();
     }
@@ -545,7 +569,7 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
     __syncwarp();
     UPP_PROF_ADD(4)
     __syncwarp();
-    if (lane == 0) mbar_arrive(emptyX);
+    if (lane == 0 && !UPP_RED) mbar_arrive(emptyX);
   }
   UPP_PROF_PRINT
   if (lane == 0) bulk_wait0();
