@@ -190,7 +190,11 @@ tsqr_status tsqr_nccl_comm_destroy(void* comm);
 /* ------------------------------------------------------------------------- */
 /* Step-level entry points (the hot-path steps of SURVEY §8(a), exposed so each */
 /* kernel can be checked against the oracle on its own).  All pointers device, */
-/* column-major, enqueued on `cuda_stream`, single GPU (no allreduce).          */
+/* column-major, enqueued on `cuda_stream`, single GPU (no allreduce).  The     */
+/* split-row entries (gram, proj, and chol_inv for b >= 128) share ONE library- */
+/* owned device scratch buffer (grown with cudaMallocAsync on the call's        */
+/* stream): call them from one host thread and one stream at a time.  The plan  */
+/* API (tsqr_create / tsqr_factor) does not use it.                             */
 /* ------------------------------------------------------------------------- */
 
 /* W (b x b, ldw >= b) = X^T X for X (m x b): the local Gram block (Alg. 2 l.2,
