@@ -56,12 +56,13 @@ def _work(rank, world, q, m_local, n, b, kappa, algo, cuts):
     from harness import verify
     comm = t.NcclComm(rank, world, rank)
     m = m_local * world
+    chunk = min(m_local, 65536)  # generator chunk of the global matrix (independent of the split)
     if cuts is None:  # equal block rows
         A = t.colmajor_empty(m_local, n, device=f"cuda:{rank}")
-        synth.generate_torch(A, m, rank * m_local, n, kappa, seed=1, chunk=min(m_local, 65536))
+        synth.generate_torch(A, m, rank * m_local, n, kappa, seed=1, chunk=chunk)
     else:  # uneven block rows [cuts[rank], cuts[rank+1]) of the same global matrix
         Af = t.colmajor_empty(m, n, device=f"cuda:{rank}")
-        synth.generate_torch(Af, m, 0, n, kappa, seed=1, chunk=min(m_local, 65536))
+        synth.generate_torch(Af, m, 0, n, kappa, seed=1, chunk=chunk)
         m_local = cuts[rank + 1] - cuts[rank]
         A = t.colmajor_empty(m_local, n, device=f"cuda:{rank}")
         A.copy_(Af[cuts[rank]:cuts[rank + 1]])
@@ -78,7 +79,7 @@ def _work(rank, world, q, m_local, n, b, kappa, algo, cuts):
     out = {"R": [r.numpy() for r in Rs], "calls": calls, "orth": orth, "res": res}
     if rank == 0:
         Af = t.colmajor_empty(m, n, device="cuda:0")
-        synth.generate_torch(Af, m, 0, n, kappa, seed=1, chunk=min(m_local, 65536))
+        synth.generate_torch(Af, m, 0, n, kappa, seed=1, chunk=chunk)
         out["R1"] = t.factor(Af, b, algo).cpu().numpy()
     plan.close()
     torch.cuda.synchronize()
@@ -103,6 +104,16 @@ def test_uneven_block_rows():
     cuts = [0] + [int(m * (r + 1) / world) + (1000 * (r + 1) if r + 1 < world else 0) - 37 * r
                   for r in range(world - 1)] + [m]
     _run_ranks("mcqr2gs", 256, 64, 1e6, cuts=cuts)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_rank_with_no_rows():
+    """A rank may own zero rows (m_local = 0): it still takes part in every allreduce with
+    zero partial sums and receives the same R."""
+    world = min(_ngpu(), 4)
+    m = world << 17
+    cuts = [0, 0] + [int(m * (r + 1) / world) for r in range(1, world - 1)] + [m]
+    _run_ranks("mcqr2gs", 128, 32, 1e6, cuts=cuts)
 
 
 def _run_ranks(algo, n, b, kappa, cuts=None):
