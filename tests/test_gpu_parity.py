@@ -315,3 +315,56 @@ def test_factor_host_equals_device_factor(T, algo, b):
     Ad = T.to_colmajor(A)
     assert np.array_equal(p.factor(Ad).cpu().numpy(), Rd)
     p.close()
+
+
+def test_full_size_cfg3_in_bench_configuration(T, orc):
+    """BASELINE configs[2] at full size (2^22 x 512, b = 64, kappa = 1e15) in the launch
+    configuration bench.py times (plan + CUDA-graph replay): the gates and invariants hold
+    at this size, and the leading block R_11 -- the CQR2 of the first panel (Alg. 8 l.1),
+    which the oracle can compute at full size -- matches the oracle to 1e-10 (the first panel
+    is well conditioned: Eq. 7 bounds its condition by the spectrum's first 64 values)."""
+    import torch
+    from harness import verify
+    m, n, b = 1 << 22, 512, 64
+    A = T.colmajor_empty(m, n)
+    synth.generate_torch(A, m, 0, n, 1e15, seed=0)
+    A1 = np.asfortranarray(A[:, :b].cpu().numpy())
+    A0 = A.clone()
+    p = T.Plan(m, n, b, "mcqr2gs")
+    R = p.factor(A)          # captures the graph
+    A.copy_(A0)
+    R = p.factor(A)          # graph replay, as in bench.py
+    p.wait()
+    orth = verify.orthogonality(A)
+    res = verify.residual(A0, A, R)
+    Rh = R.cpu().numpy()
+    p.close()
+    del A0
+    torch.cuda.empty_cache()
+    check_invariants(Rh)
+    assert orth <= 1e-13 and res <= 1e-14, (orth, res)
+    _, R11, info = orc.factor(A1, b, "cqr2")
+    assert info["status"] == 0
+    assert np.linalg.norm(Rh[:b, :b] - R11) / np.linalg.norm(R11) <= 1e-10
+
+
+def test_full_size_cfg5_r_equals_r_of_sigma_vt(T):
+    """BASELINE configs[4] at full size (CQR2, 2^24 x 128, kappa = 1e2): the generator builds
+    A = U (Sigma V^T) with U^T U = I, so R(A) = R(Sigma V^T), an n x n QR done here by LAPACK --
+    a property that holds at any m (the oracle cannot run 2^24 rows in seconds)."""
+    import torch
+    from harness import verify
+    m, n = 1 << 24, 128
+    A = T.colmajor_empty(m, n)
+    sigma, V = synth.generate_torch(A, m, 0, n, 1e2, seed=0)
+    A0 = A.clone()
+    R = T.factor(A, n, "cqr2").cpu().numpy()
+    orth = verify.orthogonality(A)
+    res = verify.residual(A0, A, torch.from_numpy(R).cuda())
+    del A0
+    torch.cuda.empty_cache()
+    check_invariants(R)
+    assert orth <= 1e-13 and res <= 1e-14, (orth, res)
+    Rb = np.linalg.qr(sigma[:, None] * V.T, mode="r")
+    Rb = Rb * np.sign(np.diag(Rb))[:, None]
+    assert np.linalg.norm(R - Rb) / np.linalg.norm(Rb) <= 1e-12
