@@ -27,7 +27,12 @@
  *     status from tsqr_create leaves *plan == NULL.
  *   - The library performs no host<->device copies of A or R, no cuBLAS/cuSOLVER
  *     calls and has no CPU fallback: every arithmetic step runs in its own sm_100a
- *     kernels.  Cross-GPU sums use NCCL allreduce (ncclFloat64, ncclSum).
+ *     kernels.  Cross-GPU sums (nranks > 1) are fused into the split-row reduction kernel:
+ *     each rank stores its block sums into every peer's slot of a symmetric NCCL window
+ *     (NCCL device API, NVLink load/store) and, after an LSA barrier, adds the nranks slots
+ *     in rank order -- deterministic and bitwise identical on every rank.  Environment
+ *     TSQR_NCCL_ALLREDUCE=1 (read at tsqr_create) uses ncclAllReduce(ncclFloat64, ncclSum)
+ *     instead.
  *
  * Citation keys: P:n = line n of the paper's LaTeX source;
  * DESIGN.md lists the readings (R-k) taken where the paper is silent.
@@ -169,7 +174,10 @@ tsqr_status tsqr_timing(tsqr_plan_t plan, int32_t kclass, double* ms, int64_t* l
  * enable = 0 switches to eager enqueueing. */
 tsqr_status tsqr_set_graph(tsqr_plan_t plan, int32_t enable);
 
-/* Destroy the plan (host state and its CUDA graph). */
+/* Destroy the plan (host state, its CUDA graph and, with nranks > 1, the symmetric NCCL
+ * window and device communicator of the fused reduce + allreduce).  COLLECTIVE when the plan
+ * has a communicator with nranks > 1: every rank destroys its plan, before the
+ * communicator. */
 tsqr_status tsqr_destroy(tsqr_plan_t plan);
 
 /* Human-readable name of a status; static storage. */

@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC_DIR = os.path.join(HERE, "csrc")
 SOURCES = [os.path.join(SRC_DIR, "tsqr.cu")]
-DEPS = SOURCES + [os.path.join(SRC_DIR, "kernels.cuh"), os.path.join(ROOT, "include", "tsqr.h")]
+DEPS = SOURCES + sorted(os.path.join(SRC_DIR, f) for f in os.listdir(SRC_DIR) if f.endswith(".cuh")) + [
+    os.path.join(ROOT, "include", "tsqr.h")]
 LIB = os.path.join(HERE, "libtsqr.so")
 
 

@@ -3,3 +3,4 @@
 #include "common.cuh"
 #include "small_kernels.cuh"
 #include "stream_kernels.cuh"
+#include "fused_allreduce.cuh"

@@ -259,9 +259,16 @@ struct Launcher {
     return TSQR_OK;
   }
 
-  // OUT (p x q, ldo) = L^T R summed over all m rows (split-row partials + fixed-order reduce)
+  // cross-GPU sum fused into the reduction (fused_allreduce.cuh); ar_on only with nranks > 1
+  bool ar_on = false;
+  ncclDevComm ar_dc{};
+  ncclWindow_t ar_win = nullptr;
+  int ar_nranks = 1, ar_rank = 0;
+
+  // OUT (p x q, ldo) = L^T R summed over all m rows (split-row partials + fixed-order reduce);
+  // with `global` and the fused path on: summed over every rank as well (one kernel)
   tsqr_status atb(const double* L, int64_t ldl, const double* R, int64_t ldr, int64_t m, int p, int q, bool gram,
-                  double* part, double* out, int ldo) {
+                  double* part, double* out, int ldo, bool global = false) {
     AtbShape sh = atb_shape(m, p, q, gram);
     ProjArgs a;
     std::memset(&a, 0, sizeof(a));
@@ -284,6 +291,17 @@ struct Launcher {
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
+    if (global && ar_on) {
+      if (gram) tend(t0, TSQR_KCLASS_GRAM, (double)m * p * p, 8.0 * m * p);
+      else tend(t0, TSQR_KCLASS_PROJ, 2.0 * m * p * q, 8.0 * m * (p + q));
+      const size_t t1 = tbegin();
+      k_reduce_allreduce<<<AR_CTAS, AR_NT, 0, st>>>(part, sh.S, sh.Sd, p, q, p, (int64_t)p * q, out, ldo,
+                                                    gram ? 1 : 0, status, ar_dc, ar_win, ar_nranks, ar_rank);
+      CUDA_TRY(cudaGetLastError());
+      launches += 1;
+      tend(t1, TSQR_KCLASS_ALLREDUCE, 0.0, 8.0 * p * q);
+      return TSQR_OK;
+    }
     TRY(reduce(part, sh.S, p, q, p, (int64_t)p * q, out, ldo, gram, sh.Sd));
     if (gram) tend(t0, TSQR_KCLASS_GRAM, (double)m * p * p, 8.0 * m * p);
     else tend(t0, TSQR_KCLASS_PROJ, 2.0 * m * p * q, 8.0 * m * (p + q));
@@ -466,6 +484,11 @@ struct tsqr_plan_s {
   int64_t glda = 0;
   int32_t gldr = 0;
   bool gtiming = false;
+  // fused reduce + cross-GPU sum: symmetric NCCL window (one p x q slot per rank) + device comm
+  void* ar_buf = nullptr;
+  ncclWindow_t ar_win = nullptr;
+  bool ar_dc_ok = false;
+  ncclDevComm ar_dc{};
   // tsqr_factor_host: per-panel "Q_j is final" events (recorded inside the graph as external
   // event nodes while capturing) so the device->host copy of Q_j overlaps the later panels
   bool panel_events = false, gpanel = false;
@@ -473,6 +496,9 @@ struct tsqr_plan_s {
   cudaStream_t d2h = nullptr;
   cudaEvent_t ev_d2h = nullptr, ev_fact = nullptr;
   ~tsqr_plan_s() {
+    if (comm && ar_dc_ok) ncclDevCommDestroy(comm, &ar_dc);
+    if (comm && ar_win) ncclCommWindowDeregister(comm, ar_win);
+    if (ar_buf) ncclMemFree(ar_buf);
     for (cudaEvent_t e : ev_panel) cudaEventDestroy(e);
     if (ev_d2h) cudaEventDestroy(ev_d2h);
     if (ev_fact) cudaEventDestroy(ev_fact);
@@ -564,7 +590,8 @@ tsqr_status panel_done(tsqr_plan_s* P, int j) {
 
 // W <- allreduce(X^T X), X = m x w slab (standalone split-row Gram)
 tsqr_status gram(tsqr_plan_s* P, const double* X, int64_t ldx, int w) {
-  TRY(P->L.atb(X, ldx, X, ldx, P->m, w, w, true, P->part, P->W, w));
+  TRY(P->L.atb(X, ldx, X, ldx, P->m, w, w, true, P->part, P->W, w, true));
+  if (P->L.ar_on) { P->allreduces++; return TSQR_OK; }
   return allreduce(P, P->W, (size_t)w * w);
 }
 
@@ -588,7 +615,8 @@ tsqr_status cqr(tsqr_plan_s* P, double* X, int64_t ldx, int w, double* Uout, int
 
 // OUT (p x q, ld p) <- allreduce(L^T Rm)
 tsqr_status proj(tsqr_plan_s* P, const double* Lm, int64_t ldl, int p, const double* Rm, int64_t ldr, int q, double* out) {
-  TRY(P->L.atb(Lm, ldl, Rm, ldr, P->m, p, q, false, P->part, out, p));
+  TRY(P->L.atb(Lm, ldl, Rm, ldr, P->m, p, q, false, P->part, out, p, true));
+  if (P->L.ar_on) { P->allreduces++; return TSQR_OK; }
   return allreduce(P, out, (size_t)p * q);
 }
 
@@ -682,6 +710,48 @@ tsqr_status run_scqr3(tsqr_plan_s* P, double* A, int64_t lda, double* R, int ldr
   return P->L.trimul(P->R2, n, P->R1, n, R, ldr, n);    // l.3: R = R2 R1
 }
 
+// Fused reduce + cross-GPU sum (fused_allreduce.cuh): a symmetric window of nranks slots of
+// the largest allreduced block (b x n) and an NCCL device communicator with AR_CTAS LSA
+// barriers.  Collective (all ranks call it from tsqr_create in the same order).  Disabled with
+// TSQR_NCCL_ALLREDUCE=1, or when the ranks are not all load/store reachable (then every
+// allreduce is ncclAllReduce).
+tsqr_status setup_fused_allreduce(tsqr_plan_s* p) {
+  const char* env = std::getenv("TSQR_NCCL_ALLREDUCE");
+  if (env && std::atoi(env) != 0) return TSQR_OK;
+  const size_t count = (size_t)p->b * (size_t)p->n;
+  size_t bytes = sizeof(double) * count * (size_t)p->nranks;
+  bytes = (bytes + 4095) / 4096 * 4096;
+  // the local allocation may fail on one rank only: agree on it (min over ranks) before the
+  // collective registration, so that every rank takes the same path
+  int32_t ok = ncclMemAlloc(&p->ar_buf, bytes) == ncclSuccess ? 1 : 0;
+  {
+    int32_t* d = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int32_t), p->stream));
+    CUDA_TRY(cudaMemcpyAsync(d, &ok, sizeof(int32_t), cudaMemcpyHostToDevice, p->stream));
+    NCCL_TRY(ncclAllReduce(d, d, 1, ncclInt32, ncclMin, p->comm, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(&ok, d, sizeof(int32_t), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    CUDA_TRY(cudaFreeAsync(d, p->stream));
+  }
+  if (!ok) {  // fall back to ncclAllReduce on every rank
+    if (p->ar_buf) ncclMemFree(p->ar_buf);
+    p->ar_buf = nullptr;
+    return TSQR_OK;
+  }
+  NCCL_TRY(ncclCommWindowRegister(p->comm, p->ar_buf, bytes, &p->ar_win, NCCL_WIN_COLL_SYMMETRIC));
+  ncclDevCommRequirements_t req = {};
+  req.lsaBarrierCount = AR_CTAS;
+  NCCL_TRY(ncclDevCommCreate(p->comm, &req, &p->ar_dc));
+  p->ar_dc_ok = true;
+  if (p->ar_dc.lsaSize != p->nranks) return TSQR_OK;  // not every rank is peer-addressable
+  p->L.ar_on = true;
+  p->L.ar_dc = p->ar_dc;
+  p->L.ar_win = p->ar_win;
+  p->L.ar_nranks = p->nranks;
+  p->L.ar_rank = p->rank;
+  return TSQR_OK;
+}
+
 const char* status_names[] = {"TSQR_OK", "TSQR_ERR_INVALID_ARG", "TSQR_ERR_UNSUPPORTED", "TSQR_ERR_CUDA",
                               "TSQR_ERR_NCCL", "TSQR_ERR_BREAKDOWN", "TSQR_ERR_WORKSPACE"};
 
@@ -764,6 +834,13 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
   p->L.st = stream;
   p->L.status = p->status;
   p->L.timer = &p->timer;
+  if (comm && nranks > 1) {
+    const tsqr_status fs = setup_fused_allreduce(p);
+    if (fs != TSQR_OK) {
+      delete p;
+      return fs;
+    }
+  }
   *plan = p;
   return TSQR_OK;
 }
