@@ -7,14 +7,16 @@
 // k_reduce_allreduce (one launch replaces k_reduce + ncclAllReduce of Alg. 2 l.3 P:154,
 // Alg. 7 l.3/l.8 P:345/Alg. 8 l.3/l.7):
 //   1. every CTA forms the local sum of the split-row partials of its 32-element groups (the
-//      fixed order of k_reduce) and stores it into slot[rank] of EVERY rank's window;
+//      fixed order of k_reduce) and stores it into slot[parity][rank] of EVERY rank's window;
 //   2. LSA barrier (acq_rel, per CTA index): all ranks' slots of these groups have landed;
-//   3. out = slot[0] + slot[1] + ... + slot[P-1] in rank order from the local window copy --
+//   3. out = slot[parity][0] + ... + slot[parity][P-1] in rank order from the local window --
 //      a fixed order, so every rank gets the same bits (R is replicated bitwise) and
-//      the result is run-to-run deterministic (unlike a library allreduce);
-//   4. second LSA barrier, so no rank overwrites a slot (next call) that a slower rank is
-//      still reading.
-// Every rank executes both barriers even after a breakdown (the status is identical on all
+//      the result is run-to-run deterministic (unlike a library allreduce).
+// parity = the barrier's epoch (number of completed syncs of this CTA index: the same on every
+// rank, persistent across CUDA-graph replays) & 1: a fast rank's next call writes the other
+// half of the window, and the call after that only starts once every rank has passed this
+// call's successor barrier, i.e. finished reading -- one barrier per call.
+// Every rank executes the barrier even after a breakdown (the status is identical on all
 // ranks because all factor the same allreduced Gram, but the barriers must still match).
 #pragma once
 #include <nccl_device.h>
@@ -34,6 +36,8 @@ __global__ void __launch_bounds__(AR_NT) k_reduce_allreduce(const double* __rest
   const bool skip = failed(status);  // uniform across CTAs and ranks
   const int64_t pq = (int64_t)p * q;
   const int64_t ngroups = (pq + 31) / 32;
+  ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x);
+  const size_t half = (size_t)(bar.epoch & 1) * (size_t)nranks * (size_t)pq;  // window half of this call
   if (!skip) {
     for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
       const int64_t e = g * 32 + lane;
@@ -52,18 +56,15 @@ __global__ void __launch_bounds__(AR_NT) k_reduce_allreduce(const double* __rest
       if (warp == 0 && live) {
         const double v = ((ws[0][lane] + ws[1][lane]) + (ws[2][lane] + ws[3][lane])) +
                          ((ws[4][lane] + ws[5][lane]) + (ws[6][lane] + ws[7][lane]));
-        const size_t off = sizeof(double) * ((size_t)rank * (size_t)pq + (size_t)e);
+        const size_t off = sizeof(double) * (half + (size_t)rank * (size_t)pq + (size_t)e);
         for (int r = 0; r < nranks; ++r) *reinterpret_cast<double*>(ncclGetLsaPointer(win, off, r)) = v;
       }
       __syncthreads();
     }
   }
-  {
-    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x);
-    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
-  }
+  bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   if (!skip && threadIdx.x < 32) {
-    const double* slots = reinterpret_cast<const double*>(ncclGetLocalPointer(win, 0));
+    const double* slots = reinterpret_cast<const double*>(ncclGetLocalPointer(win, 0)) + half;
     for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
       const int64_t e = g * 32 + lane;
       const int i = (int)(e % p), j = (int)(e / p);
@@ -74,10 +75,6 @@ __global__ void __launch_bounds__(AR_NT) k_reduce_allreduce(const double* __rest
         if (gram && i != j) out[j + (int64_t)i * ldo] = v;
       }
     }
-  }
-  {
-    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), blockIdx.x);
-    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   }
 }
 

@@ -719,7 +719,7 @@ tsqr_status setup_fused_allreduce(tsqr_plan_s* p) {
   const char* env = std::getenv("TSQR_NCCL_ALLREDUCE");
   if (env && std::atoi(env) != 0) return TSQR_OK;
   const size_t count = (size_t)p->b * (size_t)p->n;
-  size_t bytes = sizeof(double) * count * (size_t)p->nranks;
+  size_t bytes = sizeof(double) * count * (size_t)p->nranks * 2;  // two halves (call parity)
   bytes = (bytes + 4095) / 4096 * 4096;
   // the local allocation may fail on one rank only: agree on it (min over ranks) before the
   // collective registration, so that every rank takes the same path
