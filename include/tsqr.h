@@ -30,9 +30,9 @@
  *     kernels.  Cross-GPU sums (nranks > 1) are fused into the split-row reduction kernel:
  *     each rank stores its block sums into every peer's slot of a symmetric NCCL window
  *     (NCCL device API, NVLink load/store) and, after an LSA barrier, adds the nranks slots
- *     in rank order -- deterministic and bitwise identical on every rank.  Environment
- *     TSQR_NCCL_ALLREDUCE=1 (read at tsqr_create) uses ncclAllReduce(ncclFloat64, ncclSum)
- *     instead.
+ *     in rank order -- deterministic and bitwise identical on every rank (validated on 2
+ *     and 4 GPUs; with more than 4 ranks only if TSQR_FUSED_ALLREDUCE=1).  Otherwise, or with
+ *     TSQR_NCCL_ALLREDUCE=1 (read at tsqr_create), ncclAllReduce(ncclFloat64, ncclSum).
  *
  * Citation keys: P:n = line n of the paper's LaTeX source;
  * DESIGN.md lists the readings (R-k) taken where the paper is silent.

@@ -713,11 +713,15 @@ tsqr_status run_scqr3(tsqr_plan_s* P, double* A, int64_t lda, double* R, int ldr
 // Fused reduce + cross-GPU sum (fused_allreduce.cuh): a symmetric window of nranks slots of
 // the largest allreduced block (b x n) and an NCCL device communicator with AR_CTAS LSA
 // barriers.  Collective (all ranks call it from tsqr_create in the same order).  Disabled with
-// TSQR_NCCL_ALLREDUCE=1, or when the ranks are not all load/store reachable (then every
-// allreduce is ncclAllReduce).
+// TSQR_NCCL_ALLREDUCE=1, for more than 4 ranks unless TSQR_FUSED_ALLREDUCE=1, or when the
+// ranks are not all load/store reachable (then every allreduce is ncclAllReduce).
 tsqr_status setup_fused_allreduce(tsqr_plan_s* p) {
   const char* env = std::getenv("TSQR_NCCL_ALLREDUCE");
   if (env && std::atoi(env) != 0) return TSQR_OK;
+  // validated on 2 and 4 B200s of one box; larger rank counts keep ncclAllReduce unless
+  // TSQR_FUSED_ALLREDUCE=1 asks for the fused kernel
+  const char* force = std::getenv("TSQR_FUSED_ALLREDUCE");
+  if (p->nranks > 4 && !(force && std::atoi(force) != 0)) return TSQR_OK;
   const size_t count = (size_t)p->b * (size_t)p->n;
   size_t bytes = sizeof(double) * count * (size_t)p->nranks * 2;  // two halves (call parity)
   bytes = (bytes + 4095) / 4096 * 4096;
