@@ -521,7 +521,11 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
     // epilogue: X <- X - acc in the slot (all loads before any store: a store may alias a
     // later load for the compiler, and interleaving them serialises the load->add->store
     // chains), then TMA stores of 16 rows x 8*NJ columns per warp
-    if (UPP_RED) {  // slot <- -acc (sign flips on the integer pipe; the previous reduce has read it)
+    if (UPP_RED) {  // slot <- -acc (sign flips on the integer pipe)
+      // the previous chunk's reduce-add boxes must have read this warp's region: waited for
+      // here, a whole chunk of DMMAs after they were issued, instead of right after issuing
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -565,11 +569,12 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
       bulk_commit();
     }
     UPP_PROF_ADD(3)
-    if (lane == 0) bulk_wait_read0();  // the TMA stores have read the slot
-    __syncwarp();
-    UPP_PROF_ADD(4)
-    __syncwarp();
-    if (lane == 0 && !UPP_RED) mbar_arrive(emptyX);
+    if (!UPP_RED) {
+      if (lane == 0) bulk_wait_read0();  // the TMA stores have read the slot
+      __syncwarp();
+      UPP_PROF_ADD(4)
+      if (lane == 0) mbar_arrive(emptyX);
+    }
   }
   UPP_PROF_PRINT
   if (lane == 0) bulk_wait0();
