@@ -368,3 +368,27 @@ def test_full_size_cfg5_r_equals_r_of_sigma_vt(T):
     Rb = np.linalg.qr(sigma[:, None] * V.T, mode="r")
     Rb = Rb * np.sign(np.diag(Rb))[:, None]
     assert np.linalg.norm(R - Rb) / np.linalg.norm(Rb) <= 1e-12
+
+
+@pytest.mark.parametrize("kappa,seed", [(1e8, 1), (1e12, 2), (1e15, 3)])
+def test_full_size_cfg2_sweep(T, kappa, seed):
+    """BASELINE configs[1] shape at full size (2^22 x 256, b = 64) over kappa and seeds: the
+    mCQR2GS gates and invariants hold in the bench configuration (graph replay)."""
+    import torch
+    from harness import verify
+    m, n, b = 1 << 22, 256, 64
+    A = T.colmajor_empty(m, n)
+    synth.generate_torch(A, m, 0, n, kappa, seed=seed)
+    A0 = A.clone()
+    p = T.Plan(m, n, b, "mcqr2gs")
+    p.factor(A)
+    A.copy_(A0)
+    R = p.factor(A)
+    p.wait()
+    orth = verify.orthogonality(A)
+    res = verify.residual(A0, A, R)
+    check_invariants(R.cpu().numpy())
+    p.close()
+    del A0
+    torch.cuda.empty_cache()
+    assert orth <= 1e-13 and res <= 1e-14, (orth, res)
