@@ -380,18 +380,24 @@ constexpr int UPP_REG_PROD = 40;
 #define TSQR_UPP_RED 1
 #endif
 constexpr bool UPP_RED = TSQR_UPP_RED;  // epilogue: -acc through the slot + TMA reduce-add into X
-constexpr int UPP_LSL = 32 * LDT;          // L half slot (doubles)
-constexpr int UPP_LDS = 36;                // S half slot leading dimension
-constexpr int UPP_SSL = 64 * UPP_LDS;      // S half slot (doubles)
+#ifndef TSQR_UPP_KQ
+#define TSQR_UPP_KQ 32
+#endif
+constexpr int UPP_KQ = TSQR_UPP_KQ;        // k per ring slot (32: halves; 16: quarters)
+constexpr int UPP_NSL = 64 / UPP_KQ;       // ring slots (one 64-deep k chunk in flight)
+constexpr int UPP_LSL = UPP_KQ * LDT;      // L slot (doubles)
+constexpr int UPP_LDS = UPP_KQ + 4;        // S slot leading dimension (== 4 mod 16)
+constexpr int UPP_SSL = 64 * UPP_LDS;      // S slot (doubles)
 constexpr uint32_t UPP_TX = (UPP_LSL + UPP_SSL) * 8;
-constexpr int UPP_GROUP = XSLOT + 2 * UPP_LSL + 2 * UPP_SSL;  // doubles per group (multiple of 128)
-constexpr size_t UPP_SMEM = sizeof(double) * 2 * (size_t)UPP_GROUP + 12 * sizeof(uint64_t) + 1024;
+constexpr int UPP_GROUP = XSLOT + UPP_NSL * UPP_LSL + UPP_NSL * UPP_SSL;  // doubles per group
+constexpr int UPP_NBAR = 2 * UPP_NSL + 2;  // full/empty per slot + fullX/emptyX
+constexpr size_t UPP_SMEM = sizeof(double) * 2 * (size_t)UPP_GROUP + 2 * UPP_NBAR * sizeof(uint64_t) + 1024;
 
 struct UppArgs {
   CUtensorMap mapX;   // X: box (16 rows, 64 cols), 128-byte swizzle (loads)
   CUtensorMap mapXs;  // X: box (16 rows, 8*UPP_NJ cols), 128-byte swizzle (stores)
-  CUtensorMap mapL;   // L: box (68 rows, 32 cols)
-  CUtensorMap mapS;   // S: box (36 rows, 64 cols)
+  CUtensorMap mapL;   // L: box (68 rows, UPP_KQ cols)
+  CUtensorMap mapS;   // S: box (UPP_KQ + 4 rows, 64 cols)
   int64_t m;
   int p, q;
   const int* status;
@@ -424,14 +430,14 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
   const int grp = producer ? (warp - 2 * UPP_GW) & 1 : warp / UPP_GW;
   double* sX = smem + grp * UPP_GROUP;  // 1024-byte aligned (swizzled slot)
   double* ringL = sX + XSLOT;
-  double* ringS = ringL + 2 * UPP_LSL;
-  uint64_t* fullLS = bars + grp * 6;
-  uint64_t* emptyLS = fullLS + 2;
-  uint64_t* fullX = fullLS + 4;
-  uint64_t* emptyX = fullLS + 5;
+  double* ringS = ringL + UPP_NSL * UPP_LSL;
+  uint64_t* fullLS = bars + grp * UPP_NBAR;
+  uint64_t* emptyLS = fullLS + UPP_NSL;
+  uint64_t* fullX = fullLS + 2 * UPP_NSL;
+  uint64_t* emptyX = fullX + 1;
 
   const int64_t ntr = (a.m + TR - 1) / TR;
-  const int nxc = (a.q + 63) / 64, nkh = (a.p + 31) / 32;
+  const int nxc = (a.q + 63) / 64, nkh = (a.p + UPP_KQ - 1) / UPP_KQ;
   const int64_t first = blockIdx.x, stride = gridDim.x;
   const int nmine = (int)(first < ntr ? (ntr - 1 - first) / stride + 1 : 0);
   const int ntl = nmine > grp ? (nmine - 1 - grp) / 2 + 1 : 0;  // this group's row tiles
@@ -439,10 +445,12 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
 
   if (threadIdx.x == 0) {
     for (int g = 0; g < 2; ++g) {
-      uint64_t* b = bars + g * 6;
-      mbar_init(&b[0], 1); mbar_init(&b[1], 1);            // fullLS
-      mbar_init(&b[2], UPP_GW); mbar_init(&b[3], UPP_GW);  // emptyLS
-      mbar_init(&b[4], 1); mbar_init(&b[5], UPP_GW);       // fullX, emptyX
+      uint64_t* b = bars + g * UPP_NBAR;
+      for (int s = 0; s < UPP_NSL; ++s) {
+        mbar_init(&b[s], 1);                  // fullLS
+        mbar_init(&b[UPP_NSL + s], UPP_GW);   // emptyLS
+      }
+      mbar_init(&b[2 * UPP_NSL], 1); mbar_init(&b[2 * UPP_NSL + 1], UPP_GW);  // fullX, emptyX
     }
     tma_prefetch_map(&a.mapX);
     tma_prefetch_map(&a.mapXs);
@@ -459,11 +467,11 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
       const int tl = grp + 2 * (ch / nxc), xc = ch % nxc;
       const int64_t row0 = (first + (int64_t)tl * stride) * TR;
       for (int h = 0; h < nkh; ++h, ++vLS) {
-        const int sl = vLS & 1, use = vLS >> 1;
+        const int sl = vLS % UPP_NSL, use = vLS / UPP_NSL;
         if (use > 0) mbar_wait(&emptyLS[sl], (use - 1) & 1);
         mbar_arrive_expect_tx(&fullLS[sl], UPP_TX);
-        tma_load_2d(ringL + sl * UPP_LSL, &a.mapL, (int)row0, h * 32, &fullLS[sl]);
-        tma_load_2d(ringS + sl * UPP_SSL, &a.mapS, h * 32, xc * 64, &fullLS[sl]);
+        tma_load_2d(ringL + sl * UPP_LSL, &a.mapL, (int)row0, h * UPP_KQ, &fullLS[sl]);
+        tma_load_2d(ringS + sl * UPP_SSL, &a.mapS, h * UPP_KQ, xc * 64, &fullLS[sl]);
       }
       if (UPP_RED) continue;  // X is never loaded: the L2 adds -acc into it
       if (ch > 0) mbar_wait(emptyX, (ch - 1) & 1);
@@ -488,9 +496,9 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
 #pragma unroll
       for (int j = 0; j < UPP_NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int h = 0; h < nkh; ++h, ++vLS) {
-      const int sl = vLS & 1;
+      const int sl = vLS % UPP_NSL;
       UPP_PROF_T0
-      mbar_wait(&fullLS[sl], (vLS >> 1) & 1);
+      mbar_wait(&fullLS[sl], (vLS / UPP_NSL) & 1);
       UPP_PROF_ADD(1)
       const double* sL = ringL + sl * UPP_LSL + tig * LDT + wr * 32 + gid;
       const double* sS = ringS + sl * UPP_SSL + (c0 + gid) * UPP_LDS + tig;
@@ -501,9 +509,9 @@ __global__ void __launch_bounds__(UPP_NTHR, 1) k_update_pp(const __grid_constant
 #pragma unroll
       for (int j = 0; j < UPP_NJ; ++j) fb[0][j] = sS[j * 8 * UPP_LDS];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) {
+      for (int s = 0; s < UPP_KQ / 4; ++s) {
         const int cb = s & 1, nb = cb ^ 1;
-        if (s + 1 < 8) {
+        if (s + 1 < UPP_KQ / 4) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) fa[nb][i] = sL[(s + 1) * 4 * LDT + i * 8];
 #pragma unroll

@@ -373,7 +373,7 @@ struct Launcher {
       a.m = m; a.p = p; a.q = q; a.status = status;
       TRY(make_map(&a.mapX, X, m, q, ldx, 16, 64, true));
       TRY(make_map(&a.mapXs, X, m, q, ldx, 16, 8 * UPP_NJ, true));
-      TRY(make_map(&a.mapL, L, m, p, ldl, LDT, 32));
+      TRY(make_map(&a.mapL, L, m, p, ldl, LDT, UPP_KQ));
       TRY(make_map(&a.mapS, S, p, q, lds, UPP_LDS, 64));
       CUDA_TRY(set_smem(k_update_pp, UPP_SMEM));
       k_update_pp<<<grid, UPP_NTHR, UPP_SMEM, st>>>(a);
