@@ -1,13 +1,13 @@
 #!/bin/bash
 # ncu evidence for one round, ONE ncu invocation per call (run the plain command first; ncu
 # only if it exited 0):
-#   bash tools/profile.sh <tag> launches            -> launch list of our kernels (-k regex:^k_)
+#   [CONFIG=cfgN] bash tools/profile.sh <tag> launches -> launch list of our kernels (-k regex:^k_)
 #   bash tools/profile.sh <tag> full <regex> <count> -> one --set full capture of <count>
 #                                                     launches matching <regex>
 # then `python tools/profile_summary.py <tag>` here.
 TAG=${1:-run}; MODE=${2:-launches}
 mkdir -p gpurun_out
-CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --config ${CONFIG:-cfg3}"
 $CMD > gpurun_out/prof_${TAG}_plain.json 2> gpurun_out/prof_${TAG}_plain.err || exit 1
 if [ "$MODE" = launches ]; then
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
