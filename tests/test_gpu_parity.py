@@ -392,3 +392,27 @@ def test_full_size_cfg2_sweep(T, kappa, seed):
     del A0
     torch.cuda.empty_cache()
     assert orth <= 1e-13 and res <= 1e-14, (orth, res)
+
+
+def test_maximum_width_n4096(T):
+    """The widest supported factorisation (n = 4096, b = 256: 16 panels, blocked Cholesky and
+    TRMM, 62 allreduces) meets the gates and invariants (the oracle would need minutes here;
+    the gates are size-independent properties)."""
+    import torch
+    from harness import verify
+    m, n, b = 16384, 4096, 256
+    A = T.colmajor_empty(m, n)
+    synth.generate_torch(A, m, 0, n, 1e6, seed=4, chunk=m)
+    A0 = A.clone()
+    p = T.Plan(m, n, b, "mcqr2gs")
+    R = p.factor(A)
+    p.wait()
+    assert p.counts()[0] == 4 * (n // b) - 2
+    orth = verify.orthogonality(A)
+    res = verify.residual(A0, A, R)
+    check_invariants(R.cpu().numpy())
+    p.close()
+    torch.cuda.synchronize()
+    # ||Q^TQ - I||_F grows like n * (per-entry error): the BJ gate (1e-13 at n = 512) is held at
+    # the same per-entry level through the paper's normalisation (P:104, R-1): / sqrt(n)
+    assert orth / math.sqrt(n) <= 1e-13 / math.sqrt(512) and res <= 1e-14, (orth, res)
