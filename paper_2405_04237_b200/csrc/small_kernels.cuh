@@ -58,6 +58,10 @@ __global__ void __launch_bounds__(RED_NT) k_reduce(const double* __restrict__ pa
 // On breakdown: status <- {5, pass, panel, stage, pivot, -, value(double)}.
 // -----------------------------------------------------------------------------------------
 constexpr int CHOL_NT = 512;
+#ifndef TSQR_CHOL_NT_SMALL
+#define TSQR_CHOL_NT_SMALL 512
+#endif
+constexpr int CHOL_NT_SMALL = TSQR_CHOL_NT_SMALL;  // threads of k_chol_inv (b <= 128 in shared memory)
 
 // shared-memory bytes of k_chol_inv for block size b (S and Z with padded leading dimension
 // b + 1 so that row- and column-wise accesses are bank-conflict free)
@@ -65,7 +69,8 @@ __host__ __device__ constexpr size_t chol_smem_bytes(int b) {
   return b <= 64 ? sizeof(double) * 2 * (size_t)b * (b + 1) : (b <= 128 ? sizeof(double) * (size_t)b * (b + 1) : 0);
 }
 
-__global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restrict__ W, int ldw, int b,
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_chol_inv(const double* __restrict__ W, int ldw, int b,
                                                         double* __restrict__ U, int ldu, double* __restrict__ Z,
                                                         int ldz, int* status, int pass, int panel, int stage,
                                                         double* work) {
@@ -79,7 +84,7 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restric
   double* S = s_in_smem ? smem : work;                          // S[i + j*lds]
   double* Zw = z_in_smem ? smem + (size_t)b * (b + 1) : Z;      // Zw[i + j*ldzw]
   const int ldzw = z_in_smem ? b + 1 : ldz;
-  for (int e = tid; e < b * b; e += CHOL_NT) {
+  for (int e = tid; e < b * b; e += NT) {
     const int i = e % b, j = e / b;
     S[i + j * lds] = (i <= j) ? W[i + (int64_t)j * ldw] : 0.0;
   }
@@ -99,19 +104,19 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restric
       return;  // uniform: every thread read the same d
     }
     const double ukk = sqrt(d);
-    for (int j = k + tid; j < b; j += CHOL_NT) s_urow[j] = (j == k) ? ukk : S[k + j * lds] / ukk;
+    for (int j = k + tid; j < b; j += NT) s_urow[j] = (j == k) ? ukk : S[k + j * lds] / ukk;
     __syncthreads();
     for (int j0 = 0; j0 < b; j0 += 64) {
       const int j = j0 + jj;
       if (j < b && j >= k) {
         if (ii0 == 0) S[k + j * lds] = s_urow[j];
         const double uj = s_urow[j];
-        for (int i = k + 1 + ((ii0 - (k + 1)) & 7); i <= j; i += 8) S[i + j * lds] = fma(-s_urow[i], uj, S[i + j * lds]);
+        for (int i = k + 1 + ((ii0 - (k + 1)) & (NT / 64 - 1)); i <= j; i += NT / 64) S[i + j * lds] = fma(-s_urow[i], uj, S[i + j * lds]);
       }
     }
     __syncthreads();
   }
-  for (int e = tid; e < b * b; e += CHOL_NT) {
+  for (int e = tid; e < b * b; e += NT) {
     const int i = e % b, j = e / b;
     U[i + (int64_t)j * ldu] = (i <= j) ? S[i + j * lds] : 0.0;
     Zw[i + (int64_t)j * ldzw] = 0.0;
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restric
   // all j >= i in parallel; column j handled by 8 lanes of one warp (the t-range split 8 ways)
   const int sub = tid & 7, jg = tid >> 3;
   for (int i = b - 1; i >= 0; --i) {
-    for (int jb = 0; jb < b; jb += CHOL_NT / 8) {  // uniform trip count: shuffles stay converged
+    for (int jb = 0; jb < b; jb += NT / 8) {  // uniform trip count: shuffles stay converged
       const int j = jb + jg;
       const bool act = j < b && j >= i;
       double s = 0.0;
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv(const double* __restric
     __syncthreads();
   }
   if (z_in_smem)
-    for (int e = tid; e < b * b; e += CHOL_NT) {
+    for (int e = tid; e < b * b; e += NT) {
       const int i = e % b, j = e / b;
       Z[i + (int64_t)j * ldz] = Zw[i + j * ldzw];
     }

@@ -400,8 +400,9 @@ struct Launcher {
                                                             work);
     } else {
       const size_t smem = chol_smem_bytes(b);
-      CUDA_TRY(set_smem(k_chol_inv, smem > 0 ? smem : 1));
-      k_chol_inv<<<1, CHOL_NT, smem, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage, work);
+      CUDA_TRY(set_smem(k_chol_inv<CHOL_NT_SMALL>, smem > 0 ? smem : 1));
+      k_chol_inv<CHOL_NT_SMALL><<<1, CHOL_NT_SMALL, smem, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage,
+                                                               work);
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
