@@ -383,7 +383,11 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded A = U diag(sigma) V^T with log-spaced sigma, P:108)",
             "config": {"workload": desc, "config": args.config, "m_local": m_local, "m_global": m_global, "n": n,
-                       "b": b, "kappa": kappa, "algo": algo, "parallelism": f"row-sharded dp{world} (NCCL allreduce)",
+                       "b": b, "kappa": kappa, "algo": algo, "parallelism": f"row-sharded dp{world}",
+                       "data_plane": {"local": "single GPU, no exchange",
+                                      "nccl": "k_reduce + ncclAllReduce",
+                                      "fused": "k_reduce_allreduce: split-row sum fused with the cross-GPU sum "
+                                               "over NVLink peer memory (NCCL device API)"}[plan.data_plane()],
                        "l2": "inputs 8*m_local*n bytes per GPU >> 126 MB L2; A restored from A0 between steps (untimed)"},
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -174,6 +174,13 @@ tsqr_status tsqr_timing(tsqr_plan_t plan, int32_t kclass, double* ms, int64_t* l
  * enable = 0 switches to eager enqueueing. */
 tsqr_status tsqr_set_graph(tsqr_plan_t plan, int32_t enable);
 
+/* Which cross-GPU data plane the plan's allreduces use: TSQR_PLANE_LOCAL (single rank, no
+ * exchange), TSQR_PLANE_NCCL (k_reduce + ncclAllReduce) or TSQR_PLANE_FUSED (the split-row
+ * reduction fused with the cross-GPU sum over NVLink peer memory, k_reduce_allreduce).
+ * Decided collectively at tsqr_create, identical on every rank. */
+typedef enum { TSQR_PLANE_LOCAL = 0, TSQR_PLANE_NCCL = 1, TSQR_PLANE_FUSED = 2 } tsqr_plane;
+tsqr_status tsqr_data_plane(tsqr_plan_t plan, int32_t* plane);
+
 /* Destroy the plan (host state, its CUDA graph and, with nranks > 1, the symmetric NCCL
  * window and device communicator of the fused reduce + allreduce).  COLLECTIVE when the plan
  * has a communicator with nranks > 1: every rank destroys its plan, before the
@@ -199,10 +206,11 @@ tsqr_status tsqr_nccl_comm_destroy(void* comm);
 /* Step-level entry points (the hot-path steps of SURVEY §8(a), exposed so each */
 /* kernel can be checked against the oracle on its own).  All pointers device, */
 /* column-major, enqueued on `cuda_stream`, single GPU (no allreduce).  The     */
-/* split-row entries (gram, proj, and chol_inv for b >= 128) share ONE library- */
-/* owned device scratch buffer (grown with cudaMallocAsync on the call's        */
-/* stream): call them from one host thread and one stream at a time.  The plan  */
-/* API (tsqr_create / tsqr_factor) does not use it.                             */
+/* split-row entries (gram, proj, and chol_inv for b >= 128) use a library-   */
+/* owned scratch buffer, one per device; growing it synchronises the device     */
+/* (cudaDeviceSynchronize) before the old buffer is freed.  Not thread-safe:    */
+/* call the step entries from one host thread.  The plan API (tsqr_create /     */
+/* tsqr_factor) does not use it.                                                */
 /* ------------------------------------------------------------------------- */
 
 /* W (b x b, ldw >= b) = X^T X for X (m x b): the local Gram block (Alg. 2 l.2,

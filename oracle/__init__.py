@@ -66,6 +66,8 @@ def lib():
         L.orc_tri_inv.restype = None
         L.orc_matmul.argtypes = [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, ctypes.c_int, ctypes.c_int]
         L.orc_matmul.restype = None
+        L.orc_mcqr2gs_panel.argtypes = [_P, _I64, _I64, _I64, _I64, _P, _I64, ctypes.c_int, ctypes.POINTER(Info)]
+        L.orc_mcqr2gs_panel.restype = ctypes.c_int
         L.orc_sub_prod.argtypes = [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64]
         L.orc_sub_prod.restype = None
         L.orc_factor.argtypes = [_P, _I64, _I64, _I64, _I64, ctypes.c_int, _P, _I64, ctypes.POINTER(Info)]
@@ -165,12 +167,15 @@ def tri_mul(A, B):
     return C
 
 
-def matmul(A, B):
+def matmul(A, B, C=None):
+    """A @ B (plain triple loop); with C given, returns C + A @ B (the accumulate mode used for
+    R_{1:j-1,j} += C U1, R-8)."""
     A, B = _f(A), _f(B)
     p, r = A.shape
     q = B.shape[1]
-    C = np.zeros((p, q), order="F")
-    lib().orc_matmul(_p(A), p, _p(B), r, p, r, q, _p(C), p, 0, 0)
+    acc = C is not None
+    C = np.array(C, dtype=np.float64, order="F", copy=True) if acc else np.zeros((p, q), order="F")
+    lib().orc_matmul(_p(A), p, _p(B), r, p, r, q, _p(C), p, 0, 1 if acc else 0)
     return C
 
 
@@ -199,6 +204,27 @@ def factor(A, b: int, algo: str | int):
     if rc != OK:
         return None, None, d
     return Q, R, d
+
+
+def mcqr2gs_panel(Qprev, P, R_col=None):
+    """Lines 6-8 of Alg. 8 plus the R bookkeeping (R-8) for one panel P (m x b) given the
+    earlier panels' Q_{1:j-1} = Qprev (m x c0).  R_col (c0 x b) is the incoming R_{1:j-1,j}
+    (zeros if None).  Returns (Q_j, R_{1:j-1,j}, R_jj, info)."""
+    Qprev, P = _f(Qprev), _f(P)
+    m, c0 = Qprev.shape
+    b = P.shape[1]
+    X = np.asfortranarray(np.hstack([Qprev, P]))
+    n = c0 + b
+    R = np.zeros((n, n), order="F")
+    if R_col is not None:
+        R[:c0, c0:] = R_col
+    info = Info()
+    rc = lib().orc_mcqr2gs_panel(_p(X), m, m, c0, b, _p(R), n, 2, ctypes.byref(info))
+    d = info.as_dict()
+    d["status"] = rc
+    if rc != OK:
+        return None, None, None, d
+    return X[:, c0:], R[:c0, c0:].copy(), R[c0:, c0:].copy(), d
 
 
 def householder(A):

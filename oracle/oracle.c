@@ -400,25 +400,58 @@ static int cqrgs(double* X, int64_t ldx, int64_t m, int64_t n, int64_t b, double
   return ORC_OK;
 }
 
+/* Lines 6-8 of Alg. 8 for panel j plus its R bookkeeping (R-8), on the m x
+ * (c0 + bj) leading columns of X: X[:, 0:c0] holds Q_{1:j-1} (final), X[:, c0:c0+bj] holds
+ * the panel A_j after the line-3/4 projection.
+ *     U1 = CQR(A_j)  (A_j <- V1 in place)                        (l.6; R-6)
+ *     C = Q_{1:j-1}^T A_j;  A_j -= Q_{1:j-1} C                   (l.7)
+ *     U2 = CQR(A_j)  (A_j <- Q_j)                                (l.8)
+ *     R_jj = U2 U1;  R_{1:j-1,j} += C U1                         (R-8)
+ * R points at R_{1,1} (ld ldr); R_{1:j-1,j} must hold its line-5 contents on entry.  The
+ * R-8 identity this implements: A_j = V1 U1 and V1 = Q_{1:j-1} C + Q_j U2, hence
+ * A_j = Q_{1:j-1} (C U1) + Q_j (U2 U1) for ANY panel -- so for a panel with a component
+ * G = Q_{1:j-1}^T A_j along the earlier panels, R_{1:j-1,j} gains exactly G (in exact
+ * arithmetic), which is what tests pin.  `panel` (1-based) labels a breakdown. */
+int orc_mcqr2gs_panel(double* X, int64_t ldx, int64_t m, int64_t c0, int64_t bj, double* R, int64_t ldr,
+                      int panel, orc_info* info) {
+  double* Xj = X + c0 * ldx;
+  double* U1 = (double*)malloc(sizeof(double) * (size_t)(bj * bj));
+  double* U2 = (double*)malloc(sizeof(double) * (size_t)(bj * bj));
+  double* C = (double*)malloc(sizeof(double) * (size_t)((c0 > 0 ? c0 : 1) * bj));
+  int rc = ORC_OK;
+  if (!U1 || !U2 || !C) { rc = fail(info, ORC_ERR_NOMEM, 0, 0, 0); goto done; }
+  /* l.6 */
+  rc = cqr(Xj, ldx, m, bj, U1, bj, info);
+  if (rc != ORC_OK) { rc = fail(info, rc, 1, panel, 1); goto done; }
+  /* l.7 */
+  if (c0 > 0) {
+    rc = orc_atb(X, ldx, Xj, ldx, m, c0, bj, C, c0);
+    if (rc != ORC_OK) goto done;
+    orc_sub_prod(Xj, ldx, X, ldx, C, c0, m, c0, bj);
+  }
+  /* l.8 */
+  rc = cqr(Xj, ldx, m, bj, U2, bj, info);
+  if (rc != ORC_OK) { rc = fail(info, rc, 1, panel, 2); goto done; }
+  /* R assembly (R-8) */
+  orc_matmul(U2, bj, U1, bj, bj, bj, bj, R + c0 + c0 * ldr, ldr, 1, 0);
+  if (c0 > 0) orc_matmul(C, c0, U1, bj, c0, bj, bj, R + c0 * ldr, ldr, 0, 1);
+done:
+  free(U1); free(U2); free(C);
+  return rc;
+}
+
 /* mCQR2GS(X, b) (Alg. 8; R-6, R-7, R-8):
  *   [Q_1, R_11] = CQR2(A_1)                                     (l.1)
  *   for j = 2..k:
  *     Y = Q_{j-1}^T A_{:,j:k};  A_{:,j:k} -= Q_{j-1} Y           (l.3-4)
  *     R_{j-1,j:k} = Y                                             (l.5)
- *     U1 = CQR(A_j)  (A_j <- V1 in place)                         (l.6)
- *     C = Q_{1:j-1}^T A_j;  A_j -= Q_{1:j-1} C                    (l.7)
- *     U2 = CQR(A_j)  (A_j <- Q_j)                                 (l.8)
- *     R_jj = U2 U1;  R_{1:j-1,j} += C U1                          (R-8)            */
+ *     lines 6-8 and R_jj, R_{1:j-1,j}: orc_mcqr2gs_panel above      (l.6-8)  */
 static int mcqr2gs(double* X, int64_t ldx, int64_t m, int64_t n, int64_t b, double* R, int64_t ldr,
                    orc_info* info) {
   int64_t k = (n + b - 1) / b;
   int64_t b0 = (b <= n) ? b : n;
   int rc = cqr2_block(X, ldx, m, b0, R, ldr, 1, 1, info);
   if (rc != ORC_OK) return rc;
-  double* U1 = (double*)malloc(sizeof(double) * (size_t)(b * b));
-  double* U2 = (double*)malloc(sizeof(double) * (size_t)(b * b));
-  double* C = (double*)malloc(sizeof(double) * (size_t)(n * b));
-  if (!U1 || !U2 || !C) { free(U1); free(U2); free(C); return fail(info, ORC_ERR_NOMEM, 0, 0, 0); }
   for (int64_t j = 1; j < k; ++j) {
     int64_t c0 = j * b, bj = (c0 + b <= n) ? b : n - c0;
     int64_t cp = c0 - b; /* previous panel, width b */
@@ -427,22 +460,10 @@ static int mcqr2gs(double* X, int64_t ldx, int64_t m, int64_t n, int64_t b, doub
     rc = orc_atb(X + cp * ldx, ldx, X + c0 * ldx, ldx, m, b, n - c0, Y, ldr);
     if (rc != ORC_OK) break;
     orc_sub_prod(X + c0 * ldx, ldx, X + cp * ldx, ldx, Y, ldr, m, b, n - c0);
-    /* l.6 */
-    double* Xj = X + c0 * ldx;
-    rc = cqr(Xj, ldx, m, bj, U1, bj, info);
-    if (rc != ORC_OK) { rc = fail(info, rc, 1, (int)j + 1, 1); break; }
-    /* l.7 */
-    rc = orc_atb(X, ldx, Xj, ldx, m, c0, bj, C, c0);
+    /* l.6-8 + R assembly */
+    rc = orc_mcqr2gs_panel(X, ldx, m, c0, bj, R, ldr, (int)j + 1, info);
     if (rc != ORC_OK) break;
-    orc_sub_prod(Xj, ldx, X, ldx, C, c0, m, c0, bj);
-    /* l.8 */
-    rc = cqr(Xj, ldx, m, bj, U2, bj, info);
-    if (rc != ORC_OK) { rc = fail(info, rc, 1, (int)j + 1, 2); break; }
-    /* R assembly (R-8) */
-    orc_matmul(U2, bj, U1, bj, bj, bj, bj, R + c0 + c0 * ldr, ldr, 1, 0);
-    orc_matmul(C, c0, U1, bj, c0, bj, bj, R + c0 * ldr, ldr, 0, 1);
   }
-  free(U1); free(U2); free(C);
   return rc;
 }
 

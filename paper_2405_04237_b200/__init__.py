@@ -22,13 +22,14 @@ ALGOS = {"cqr2": CQR2, "cqr2gs": CQR2GS, "mcqr2gs": MCQR2GS, "cqr": CQR, "cqrgs"
          "scqr": SCQR}
 TSQR_OK, TSQR_ERR_INVALID_ARG, TSQR_ERR_UNSUPPORTED, TSQR_ERR_CUDA = 0, 1, 2, 3
 TSQR_ERR_NCCL, TSQR_ERR_BREAKDOWN, TSQR_ERR_WORKSPACE = 4, 5, 6
+PLANES = ["local", "nccl", "fused"]
 KCLASSES = ["gram", "proj", "update", "trmm", "chol", "small", "allreduce"]
 
 LIB_PATH = os.environ.get("TSQR_LIB", _build.LIB)  # override: timing experiments only
 
 #: every function declared in include/tsqr.h
 EXPORTS = ["tsqr_workspace_bytes", "tsqr_create", "tsqr_factor", "tsqr_wait", "tsqr_last_counts",
-           "tsqr_factor_host", "tsqr_set_graph", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
+           "tsqr_factor_host", "tsqr_set_graph", "tsqr_data_plane", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
            "tsqr_nccl_comm_init", "tsqr_nccl_comm_destroy", "tsqr_gram", "tsqr_proj", "tsqr_update",
            "tsqr_chol_inv", "tsqr_trmm"]
 
@@ -74,6 +75,7 @@ def load(build_if_missing: bool = False):
     L.tsqr_factor_host.argtypes = [_VP, _VP, _I64, _VP, _I32, _VP, _I64, _VP, _I32]
     L.tsqr_set_timing.argtypes = [_VP, _I32]
     L.tsqr_set_graph.argtypes = [_VP, _I32]
+    L.tsqr_data_plane.argtypes = [_VP, ctypes.POINTER(_I32)]
     L.tsqr_timing_reset.argtypes = [_VP]
     L.tsqr_timing.argtypes = [_VP, _I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -216,6 +218,12 @@ class Plan:
 
     def set_graph(self, on: bool = True):
         _check(load().tsqr_set_graph(self.handle, 1 if on else 0), "tsqr_set_graph")
+
+    def data_plane(self) -> str:
+        """'local' (one rank), 'nccl' (k_reduce + ncclAllReduce) or 'fused' (k_reduce_allreduce)."""
+        v = _I32()
+        _check(load().tsqr_data_plane(self.handle, ctypes.byref(v)), "tsqr_data_plane")
+        return PLANES[v.value]
 
     def set_timing(self, on: bool = True):
         _check(load().tsqr_set_timing(self.handle, 1 if on else 0), "tsqr_set_timing")

@@ -59,7 +59,20 @@ void set_err(const char* fmt, ...) {
     if (s_ != TSQR_OK) return s_;       \
   } while (0)
 
-constexpr int kSMs = 148;       // B200
+// SM count of the current device (148 on B200), queried once per process: the split-row
+// partition below is a function of (m, p, q, SM count) only, so it is identical on every rank
+// of a homogeneous node.
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      n = v;
+    else
+      n = 148;
+  }
+  return n;
+}
 constexpr size_t kAlign = 256;
 
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
@@ -98,6 +111,7 @@ AtbShape atb_shape(int64_t m, int p, int q, bool gram) {
   s.tiles = nd + nf;
   const int64_t ntr = (m + TR - 1) / TR;
   const double wd = 576.0 / 1024.0;
+  const int kSMs = sm_count();
   double unit = (double)kSMs / (nd * wd + nf);                      // splits per full tile
   if (unit < 4.0) {
     // few splits: choose the multiplier with the best wave efficiency (weighted CTA work)
@@ -125,7 +139,7 @@ size_t atb_part_doubles(int64_t m, int p, int q, bool gram) {
 
 int grid_1d(int64_t n, int nt = 256) {
   int64_t g = (n + nt - 1) / nt;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 4 * kSMs));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 4 * sm_count()));
 }
 
 // ---- TMA tensor maps (cuTensorMapEncodeTiled fetched through the runtime: no -lcuda) ----
@@ -251,7 +265,7 @@ struct Launcher {
   tsqr_status reduce(const double* part, int S, int p, int q, int ldp, int64_t pstride, double* out, int ldo,
                      bool gram, int Sdiag = -1) {
     const int64_t groups = ((int64_t)p * q + 31) / 32;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, 8 * kSMs));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, 8 * sm_count()));
     k_reduce<<<grid, RED_NT, 0, st>>>(part, S, Sdiag < 0 ? S : Sdiag, p, q, ldp, pstride, out, ldo, gram ? 1 : 0,
                                       status);
     CUDA_TRY(cudaGetLastError());
@@ -264,6 +278,7 @@ struct Launcher {
   ncclDevComm ar_dc{};
   ncclWindow_t ar_win = nullptr;
   int ar_nranks = 1, ar_rank = 0;
+  int64_t ar_cap = 0;  // doubles per rank slot of the window (b * n: the largest summed block)
 
   // OUT (p x q, ldo) = L^T R summed over all m rows (split-row partials + fixed-order reduce);
   // with `global` and the fused path on: summed over every rank as well (one kernel)
@@ -296,7 +311,7 @@ struct Launcher {
       else tend(t0, TSQR_KCLASS_PROJ, 2.0 * m * p * q, 8.0 * m * (p + q));
       const size_t t1 = tbegin();
       k_reduce_allreduce<<<AR_CTAS, AR_NT, 0, st>>>(part, sh.S, sh.Sd, p, q, p, (int64_t)p * q, out, ldo,
-                                                    gram ? 1 : 0, status, ar_dc, ar_win, ar_nranks, ar_rank);
+                                                    gram ? 1 : 0, status, ar_dc, ar_win, ar_nranks, ar_rank, ar_cap);
       CUDA_TRY(cudaGetLastError());
       launches += 1;
       tend(t1, TSQR_KCLASS_ALLREDUCE, 0.0, 8.0 * p * q);
@@ -312,7 +327,7 @@ struct Launcher {
   template <int B>
   tsqr_status trmm_b(double* X, int64_t ldx, int64_t m, const double* Z, int ldz) {
     using C = TrmmCfg<B>;
-    const int grid = kSMs;
+    const int grid = sm_count();
     TrmmArgs a;
     std::memset(&a, 0, sizeof(a));
     a.X = X; a.ldx = ldx; a.m = m; a.Z = Z; a.ldz = ldz; a.status = status;
@@ -364,7 +379,7 @@ struct Launcher {
   // X (m x q) -= L (m x p) S (p x q)
   tsqr_status update(double* X, int64_t ldx, const double* L, int64_t ldl, const double* S, int64_t lds, int64_t m,
                      int p, int q) {
-    const int grid = kSMs;
+    const int grid = sm_count();
     const bool tma = tma_ok(X, ldx, m) && tma_ok(L, ldl, m) && tma_ok(S, lds, p);
     const size_t t0 = tbegin();
     if (tma) {
@@ -497,6 +512,12 @@ struct tsqr_plan_s {
   cudaStream_t d2h = nullptr;
   cudaEvent_t ev_d2h = nullptr, ev_fact = nullptr;
   ~tsqr_plan_s() {
+    // tsqr_factor is asynchronous: a graph replay (or the host copies of tsqr_factor_host) may
+    // still be running and touching the peer window -- drain every stream the plan enqueued on
+    // before releasing the window, the device communicator and the graph
+    if (gstream) cudaStreamSynchronize(gstream);
+    if (d2h) cudaStreamSynchronize(d2h);
+    cudaStreamSynchronize(stream);
     if (comm && ar_dc_ok) ncclDevCommDestroy(comm, &ar_dc);
     if (comm && ar_win) ncclCommWindowDeregister(comm, ar_win);
     if (ar_buf) ncclMemFree(ar_buf);
@@ -559,6 +580,8 @@ size_t carve(Carve& c, tsqr_plan_s* p, int64_t m, int n, int b, tsqr_algo algo) 
 
 tsqr_status check_shape(int64_t m_local, int n, int b, tsqr_algo algo) {
   if (m_local < 0 || n < 1 || n > 4096) { set_err("bad m_local/n"); return TSQR_ERR_INVALID_ARG; }
+  // TMA tensor coordinates are 32-bit row indices
+  if (m_local >= (int64_t(1) << 31)) { set_err("m_local >= 2^31 rows per rank unsupported"); return TSQR_ERR_UNSUPPORTED; }
   if (algo < TSQR_CQR2 || algo > TSQR_SCQR) { set_err("bad algo"); return TSQR_ERR_INVALID_ARG; }
   if (!valid_b(b)) { set_err("panel_b=%d not in {16,32,64,128,256}", b); return TSQR_ERR_UNSUPPORTED; }
   if (n % b != 0) { set_err("ragged panels (n %% b != 0) unsupported"); return TSQR_ERR_UNSUPPORTED; }
@@ -711,24 +734,25 @@ tsqr_status run_scqr3(tsqr_plan_s* P, double* A, int64_t lda, double* R, int ldr
   return P->L.trimul(P->R2, n, P->R1, n, R, ldr, n);    // l.3: R = R2 R1
 }
 
-// Fused reduce + cross-GPU sum (fused_allreduce.cuh): a symmetric window of nranks slots of
-// the largest allreduced block (b x n) and an NCCL device communicator with AR_CTAS LSA
-// barriers.  Collective (all ranks call it from tsqr_create in the same order).  Disabled with
-// TSQR_NCCL_ALLREDUCE=1, for more than 4 ranks unless TSQR_FUSED_ALLREDUCE=1, or when the
-// ranks are not all load/store reachable (then every allreduce is ncclAllReduce).
+// Fused reduce + cross-GPU sum (fused_allreduce.cuh): a symmetric window of 2 halves x nranks
+// slots of the largest allreduced block (b x n doubles) and an NCCL device communicator with
+// AR_CTAS LSA barriers.  Collective (all ranks call it from tsqr_create in the same order).
+// Each rank's wish (TSQR_NCCL_ALLREDUCE=1 disables it; more than 4 ranks need
+// TSQR_FUSED_ALLREDUCE=1) and its local allocation are folded into ONE min-allreduce before any
+// other collective, so ranks whose environments differ still all take the same path.  A
+// 1-rank communicator uses the fused kernel only with TSQR_FUSED_ALLREDUCE=1 (a test knob: it
+// puts k_reduce_allreduce under a single-GPU test).  The plan falls back to ncclAllReduce when
+// any rank cannot, or when the ranks are not all load/store reachable.
 tsqr_status setup_fused_allreduce(tsqr_plan_s* p) {
   const char* env = std::getenv("TSQR_NCCL_ALLREDUCE");
-  if (env && std::atoi(env) != 0) return TSQR_OK;
-  // validated on 2 and 4 B200s of one box; larger rank counts keep ncclAllReduce unless
-  // TSQR_FUSED_ALLREDUCE=1 asks for the fused kernel
   const char* force = std::getenv("TSQR_FUSED_ALLREDUCE");
-  if (p->nranks > 4 && !(force && std::atoi(force) != 0)) return TSQR_OK;
-  const size_t count = (size_t)p->b * (size_t)p->n;
+  const bool forced = force && std::atoi(force) != 0;
+  // validated on 2 and 4 B200s of one box; larger rank counts keep ncclAllReduce unless forced
+  const bool want = !(env && std::atoi(env) != 0) && (p->nranks > 1 ? (p->nranks <= 4 || forced) : forced);
+  const size_t count = (size_t)p->b * (size_t)p->n;  // cap: Gram b*b, Y b*(n-b), C (n-b)*b <= b*n
   size_t bytes = sizeof(double) * count * (size_t)p->nranks * 2;  // two halves (call parity)
   bytes = (bytes + 4095) / 4096 * 4096;
-  // the local allocation may fail on one rank only: agree on it (min over ranks) before the
-  // collective registration, so that every rank takes the same path
-  int32_t ok = ncclMemAlloc(&p->ar_buf, bytes) == ncclSuccess ? 1 : 0;
+  int32_t ok = (want && ncclMemAlloc(&p->ar_buf, bytes) == ncclSuccess) ? 1 : 0;
   {
     int32_t* d = nullptr;
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int32_t), p->stream));
@@ -754,6 +778,7 @@ tsqr_status setup_fused_allreduce(tsqr_plan_s* p) {
   p->L.ar_win = p->ar_win;
   p->L.ar_nranks = p->nranks;
   p->L.ar_rank = p->rank;
+  p->L.ar_cap = (int64_t)count;
   return TSQR_OK;
 }
 
@@ -839,7 +864,7 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
   p->L.st = stream;
   p->L.status = p->status;
   p->L.timer = &p->timer;
-  if (comm && nranks > 1) {
+  if (comm) {
     const tsqr_status fs = setup_fused_allreduce(p);
     if (fs != TSQR_OK) {
       delete p;
@@ -1088,6 +1113,12 @@ tsqr_status tsqr_timing(tsqr_plan_t P, int32_t kclass, double* ms, int64_t* laun
   return TSQR_OK;
 }
 
+tsqr_status tsqr_data_plane(tsqr_plan_t P, int32_t* plane) {
+  if (!P || !plane) return TSQR_ERR_INVALID_ARG;
+  *plane = P->L.ar_on ? TSQR_PLANE_FUSED : ((P->comm && P->nranks > 1) ? TSQR_PLANE_NCCL : TSQR_PLANE_LOCAL);
+  return TSQR_OK;
+}
+
 tsqr_status tsqr_destroy(tsqr_plan_t P) {
   delete P;
   return TSQR_OK;
@@ -1119,21 +1150,37 @@ tsqr_status tsqr_nccl_comm_destroy(void* comm) {
 }
 
 // ---- step-level entry points (single GPU) ----
+// One scratch buffer per device (the split-row partials of tsqr_gram / tsqr_proj and the
+// blocked Cholesky's work matrix).  Growing it synchronises the device first, so no kernel
+// still reading the old buffer on any stream can see it freed; released at process exit.
 namespace {
 struct Scratch {
-  double* part = nullptr;
-  size_t cap = 0;
-  ~Scratch() {}
+  static constexpr int kMaxDev = 64;
+  double* part[kMaxDev] = {};
+  size_t cap[kMaxDev] = {};
+  ~Scratch() {
+    for (int d = 0; d < kMaxDev; ++d)
+      if (part[d]) cudaFree(part[d]);  // errors ignored: the context may already be gone
+  }
 };
-thread_local Scratch g_scratch;
+Scratch g_scratch;
 
 tsqr_status scratch(size_t doubles, cudaStream_t st, double** out) {
-  if (g_scratch.cap < doubles) {
-    if (g_scratch.part) CUDA_TRY(cudaFreeAsync(g_scratch.part, st));
-    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&g_scratch.part), doubles * sizeof(double), st));
-    g_scratch.cap = doubles;
+  (void)st;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= Scratch::kMaxDev) { set_err("device index %d out of range", dev); return TSQR_ERR_INVALID_ARG; }
+  if (g_scratch.cap[dev] < doubles) {
+    if (g_scratch.part[dev]) {
+      CUDA_TRY(cudaDeviceSynchronize());
+      CUDA_TRY(cudaFree(g_scratch.part[dev]));
+      g_scratch.part[dev] = nullptr;
+      g_scratch.cap[dev] = 0;
+    }
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&g_scratch.part[dev]), doubles * sizeof(double)));
+    g_scratch.cap[dev] = doubles;
   }
-  *out = g_scratch.part;
+  *out = g_scratch.part[dev];
   return TSQR_OK;
 }
 }  // namespace

@@ -12,7 +12,7 @@ For m <= chunk this is exactly "U and V ... obtained from the SVD of a random in
 matrix" in distribution (Haar-distributed orthonormal factors).
 """
 from .matrices import (spectrum, generate_np, generate_torch, right_factor, chunk_rows,
-                       identity_scaled, integer_matrix)
+                       identity_scaled, integer_matrix, generate_panel_conditioned_np, orthonormal_np)
 
 __all__ = ["spectrum", "generate_np", "generate_torch", "right_factor", "chunk_rows",
-           "identity_scaled", "integer_matrix"]
+           "identity_scaled", "integer_matrix", "generate_panel_conditioned_np", "orthonormal_np"]

@@ -114,3 +114,30 @@ def integer_matrix(m: int, n: int, seed: int = 0, lo: int = -3, hi: int = 3) -> 
     """Small-integer entries in [lo, hi]: every product and partial sum of a Gram or
     projection over m <= 2^40 rows is an exact integer below 2^53 (exact-arithmetic pin)."""
     return np.asfortranarray(_rng(seed, 99).integers(lo, hi + 1, size=(m, n)).astype(np.float64))
+
+
+def generate_panel_conditioned_np(m: int, n: int, b: int, panel_kappas, seed: int = 0):
+    """m x n matrix whose panels (b columns each) are mutually orthogonal in exact arithmetic,
+    panel j having its own planted condition number panel_kappas[j]:
+        A = U blockdiag(Sigma_1 V_1^T, ..., Sigma_k V_k^T),  U^T U = I (m x n, Haar),
+    Sigma_j = spectrum(b, panel_kappas[j]), V_j Haar b x b.  Used to make the rounding-level
+    terms of the mCQR2GS R assembly (R-8) large: after the line-3 projection panel j keeps a
+    component ~u along Q_{1:j-1}, which the first CQR's U1^{-1} amplifies by kappa_j.
+    Returns (A, [sigma_j]).  Contains no CholeskyQR arithmetic (numpy QR draws Haar factors)."""
+    k = n // b
+    if k * b != n or len(panel_kappas) != k:
+        raise ValueError("need n = k b and one kappa per panel")
+    U = _signed_q(_rng(seed, 7, 1).standard_normal((m, n)))
+    B = np.zeros((n, n))
+    sig = []
+    for j, kap in enumerate(panel_kappas):
+        s = spectrum(b, kap)
+        Vj = _signed_q(_rng(seed, 7, 2 + j).standard_normal((b, b)))
+        B[j * b:(j + 1) * b, j * b:(j + 1) * b] = s[:, None] * Vj.T
+        sig.append(s)
+    return np.asfortranarray(U @ B), sig
+
+
+def orthonormal_np(m: int, n: int, seed: int = 0) -> np.ndarray:
+    """m x n Haar matrix with orthonormal columns (kappa = 1)."""
+    return np.asfortranarray(_signed_q(_rng(seed, 8).standard_normal((m, n))))

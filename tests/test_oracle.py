@@ -427,3 +427,62 @@ def test_scqr3_allreduce_count(orc):
     orc.reset_reduction_count()
     _, _, info = orc.factor(A, 32, "scqr3")
     assert info["status"] == 0 and orc.reduction_count() == 3
+
+
+# ---------------------------------------------------------------- round-2 pins
+def test_spec_matmul_and_accumulate_exact(orc):
+    """orc_matmul's general mode, used for R := R2 R1 and for R_{1:j-1,j} += C U1 (R-8):
+    SPEC's printed examples and an integer-exact accumulate case against int64."""
+    for ex in GOLD["matmul"]:
+        assert np.array_equal(orc.matmul(M(ex["a"]), M(ex["b"])), M(ex["expect"])), ex["cite"]
+    A = synth.integer_matrix(37, 23, seed=21)
+    B = synth.integer_matrix(23, 11, seed=22)
+    C0 = synth.integer_matrix(37, 11, seed=23)
+    want = C0.astype(np.int64) + A.astype(np.int64) @ B.astype(np.int64)
+    got = orc.matmul(A, B, C=C0)
+    assert np.array_equal(got, want.astype(np.float64))
+    assert np.array_equal(orc.matmul(A, B), (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float64))
+
+
+@pytest.mark.parametrize("m,c0,b", [(4096, 48, 16), (2048, 64, 32)])
+def test_mcqr2gs_panel_r_assembly_closed_form(orc, m, c0, b):
+    """Alg. 8 lines 6-8 with the R bookkeeping of R-8 on a panel that is NOT orthogonal to the
+    earlier panels.  Mathematics fixes the answer for any panel P: A_j = V1 U1 and
+    V1 = Q_{1:j-1} C + Q_j U2, so R_{1:j-1,j} gains exactly Q_{1:j-1}^T P and R_jj is the R
+    factor of the projected panel (I - Q Q^T) P (LAPACK, sign-normalised).  Inside the full
+    algorithm the earlier lines make Q_{1:j-1}^T P a rounding-level quantity, which is why the
+    C U1 term cannot be seen there; here it is O(1), so dropping it, flipping its sign or
+    transposing an operand fails by orders of magnitude."""
+    rng = np.random.default_rng(31)
+    Qprev = np.asfortranarray(np.linalg.qr(rng.standard_normal((m, c0)))[0])
+    N, _, _ = synth.generate_np(m, b, 1e3, seed=32, chunk=m)
+    G = rng.standard_normal((c0, b)) * 4.0
+    P = np.asfortranarray(Qprev @ G + N)
+    Y0 = rng.standard_normal((c0, b))
+    Qj, Rcol, Rjj, info = orc.mcqr2gs_panel(Qprev, P, R_col=Y0)
+    assert info["status"] == 0
+    want_col = Y0 + Qprev.T @ P
+    assert np.linalg.norm(Rcol - want_col) <= 1e-12 * np.linalg.norm(want_col)
+    Pp = P - Qprev @ (Qprev.T @ P)
+    Qh, Rh = np.linalg.qr(Pp)
+    Rh = np.sign(np.diag(Rh))[:, None] * Rh
+    assert np.linalg.norm(Rjj - Rh) <= 1e-12 * np.linalg.norm(Rh)
+    # the panel identity itself: P = Q_{1:j-1} (R_{1:j-1,j} - Y0) + Q_j R_jj
+    assert np.linalg.norm(P - Qprev @ (Rcol - Y0) - Qj @ Rjj) <= 1e-14 * np.linalg.norm(P)
+    # one block-GS pass against an O(1) component: cross-orthogonality at the u * kappa(P) level
+    assert np.linalg.norm(Qprev.T @ Qj) <= 1e-9
+
+
+def test_scqr_shift_value_closed_form(orc):
+    """The value of the sCQR shift (Alg. 4 l.2: s = sqrt(m) u ||A||_F^2, m the row
+    count, u = 2^-53).  For A with orthonormal columns G = I + O(u) and ||A||_F^2 = n, so
+    W = (1 + s) I and every R_ii^2 - 1 = s = sqrt(m) u n.  At m = 2^18, n = 64, s = 32768 u:
+    the rounding of G and R (a few u) is resolved to well under 1%; sqrt(b) for sqrt(m),
+    ||A||_F for ||A||_F^2 or u = 2^-52 are off by 2x or more."""
+    m, n = 1 << 18, 64
+    A = synth.orthonormal_np(m, n, seed=1)
+    Q, R, info = orc.factor(A, n, "scqr")
+    assert info["status"] == 0
+    s = math.sqrt(m) * U_RND * n
+    d = np.diag(R) ** 2 - 1.0
+    assert np.max(np.abs(d / s - 1.0)) <= 0.01, (d.min() / s, d.max() / s)
