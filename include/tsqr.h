@@ -33,6 +33,8 @@
  *     in rank order -- deterministic and bitwise identical on every rank (validated on 2
  *     and 4 GPUs; with more than 4 ranks only if TSQR_FUSED_ALLREDUCE=1).  Otherwise, or with
  *     TSQR_NCCL_ALLREDUCE=1 (read at tsqr_create), ncclAllReduce(ncclFloat64, ncclSum).
+ *     A plan given a 1-rank communicator runs ncclAllReduce (a copy), or the fused kernel
+ *     with TSQR_FUSED_ALLREDUCE=1 -- so both cross-GPU data planes run on one GPU in tests.
  *
  * Citation keys: P:n = line n of the paper's LaTeX source;
  * DESIGN.md lists the readings (R-k) taken where the paper is silent.
@@ -174,8 +176,8 @@ tsqr_status tsqr_timing(tsqr_plan_t plan, int32_t kclass, double* ms, int64_t* l
  * enable = 0 switches to eager enqueueing. */
 tsqr_status tsqr_set_graph(tsqr_plan_t plan, int32_t enable);
 
-/* Which cross-GPU data plane the plan's allreduces use: TSQR_PLANE_LOCAL (single rank, no
- * exchange), TSQR_PLANE_NCCL (k_reduce + ncclAllReduce) or TSQR_PLANE_FUSED (the split-row
+/* Which cross-GPU data plane the plan's allreduces use: TSQR_PLANE_LOCAL (no communicator,
+ * no exchange), TSQR_PLANE_NCCL (k_reduce + ncclAllReduce) or TSQR_PLANE_FUSED (the split-row
  * reduction fused with the cross-GPU sum over NVLink peer memory, k_reduce_allreduce).
  * Decided collectively at tsqr_create, identical on every rank. */
 typedef enum { TSQR_PLANE_LOCAL = 0, TSQR_PLANE_NCCL = 1, TSQR_PLANE_FUSED = 2 } tsqr_plane;

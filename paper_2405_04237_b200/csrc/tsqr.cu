@@ -273,7 +273,7 @@ struct Launcher {
     return TSQR_OK;
   }
 
-  // cross-GPU sum fused into the reduction (fused_allreduce.cuh); ar_on only with nranks > 1
+  // cross-GPU sum fused into the reduction (fused_allreduce.cuh); ar_on with 2-4 ranks (or forced)
   bool ar_on = false;
   ncclDevComm ar_dc{};
   ncclWindow_t ar_win = nullptr;
@@ -594,7 +594,7 @@ tsqr_status check_shape(int64_t m_local, int n, int b, tsqr_algo algo) {
 
 // ---- algorithm building blocks (plan-level, include the allreduce) ----
 tsqr_status allreduce(tsqr_plan_s* P, double* buf, size_t count) {
-  if (P->comm && P->nranks > 1) {
+  if (P->comm) {  // a 1-rank communicator runs the collective too (it is a copy): the 'nccl' plane under test
     const size_t t0 = P->L.tbegin();
     NCCL_TRY(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, P->comm, P->L.st));
     P->L.tend(t0, TSQR_KCLASS_ALLREDUCE, 0.0, 8.0 * count);
@@ -1115,7 +1115,7 @@ tsqr_status tsqr_timing(tsqr_plan_t P, int32_t kclass, double* ms, int64_t* laun
 
 tsqr_status tsqr_data_plane(tsqr_plan_t P, int32_t* plane) {
   if (!P || !plane) return TSQR_ERR_INVALID_ARG;
-  *plane = P->L.ar_on ? TSQR_PLANE_FUSED : ((P->comm && P->nranks > 1) ? TSQR_PLANE_NCCL : TSQR_PLANE_LOCAL);
+  *plane = P->L.ar_on ? TSQR_PLANE_FUSED : (P->comm ? TSQR_PLANE_NCCL : TSQR_PLANE_LOCAL);
   return TSQR_OK;
 }
 
