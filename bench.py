@@ -312,7 +312,7 @@ def main():
 
     # ---- roofline of the dominant kernel class (CUDA events inside the timed region)
     ridge = peaks["fp64_tflops_sustained"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
-    heavy = {k: v for k, v in kern.items() if k in ("gram", "proj", "update", "trmm") and v["launches"]}
+    heavy = {k: v for k, v in kern.items() if k in ("gram", "proj", "update", "trmm", "cluster") and v["launches"]}
     dom = max(heavy, key=lambda k: heavy[k]["ms"]) if heavy else None
     roof = None
     if dom:
@@ -394,6 +394,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": launches * args.steps,
             "allreduces_per_step": allreduces,
+            "exec_path": plan.exec_path(),
             "clocks": clk,
             "rows_per_s": m_global * args.steps / (total_ms / 1e3),
             "per_gpu_tflops": value / world,

@@ -150,7 +150,8 @@ tsqr_status tsqr_factor_host(tsqr_plan_t plan, double* A_host, int64_t lda_host,
  * launch of the next tsqr_factor calls (off by default; enabling it adds two event
  * records per launch).  Classes (TSQR_KCLASS_*): 0 Gram (split-row partials + reduce),
  * 1 projection (Y, C), 2 trailing/re-orth update, 3 TRMM (Q = A U^{-1}), 4 Cholesky +
- * inverse, 5 R assembly and other small kernels, 6 allreduce (NCCL).
+ * inverse, 5 R assembly and other small kernels, 6 allreduce (NCCL), 7 the single-launch
+ * cluster factorisation of small problems (tsqr_exec_path == TSQR_PATH_CLUSTER).
  * tsqr_timing synchronises the stream and returns, summed over every launch of `kclass`
  * since the last tsqr_timing_reset: total milliseconds, launch count, and the
  * ALGORITHMIC flops and HBM bytes of those launches (paper's flop counts: Gram m b^2,
@@ -163,7 +164,8 @@ typedef enum {
   TSQR_KCLASS_CHOL = 4,
   TSQR_KCLASS_SMALL = 5,
   TSQR_KCLASS_ALLREDUCE = 6,
-  TSQR_KCLASS_COUNT = 7
+  TSQR_KCLASS_CLUSTER = 7,
+  TSQR_KCLASS_COUNT = 8
 } tsqr_kclass;
 tsqr_status tsqr_set_timing(tsqr_plan_t plan, int32_t enable);
 tsqr_status tsqr_timing_reset(tsqr_plan_t plan);
@@ -182,6 +184,18 @@ tsqr_status tsqr_set_graph(tsqr_plan_t plan, int32_t enable);
  * Decided collectively at tsqr_create, identical on every rank. */
 typedef enum { TSQR_PLANE_LOCAL = 0, TSQR_PLANE_NCCL = 1, TSQR_PLANE_FUSED = 2 } tsqr_plane;
 tsqr_status tsqr_data_plane(tsqr_plan_t plan, int32_t* plane);
+
+/* Which execution path the plan's tsqr_factor takes (decided at tsqr_create):
+ * TSQR_PATH_STREAM  -- one sm_100a kernel per step of the algorithm (split-row Gram and
+ *                      projection, Cholesky, TRMM, update, R assembly), replayed as a CUDA graph;
+ * TSQR_PATH_CLUSTER -- small problems on one rank (no communicator) whose m x n matrix fits in
+ *                      the distributed shared memory of one thread-block cluster (16 CTAs, or 8):
+ *                      the whole factorisation in ONE kernel launch, A read once and Q written
+ *                      once (the paper's steps in the same order; Q = A U^{-1} as the row-wise
+ *                      triangular solve of P:122).  b in {16, 32, 64}.  TSQR_CLUSTER_PATH=0 in
+ *                      the environment at tsqr_create disables it. */
+typedef enum { TSQR_PATH_STREAM = 0, TSQR_PATH_CLUSTER = 1 } tsqr_path;
+tsqr_status tsqr_exec_path(tsqr_plan_t plan, int32_t* path);
 
 /* Destroy the plan (host state, its CUDA graph and, with nranks > 1, the symmetric NCCL
  * window and device communicator of the fused reduce + allreduce).  COLLECTIVE when the plan

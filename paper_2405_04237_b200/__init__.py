@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 
 from . import build as _build
 
@@ -23,13 +24,14 @@ ALGOS = {"cqr2": CQR2, "cqr2gs": CQR2GS, "mcqr2gs": MCQR2GS, "cqr": CQR, "cqrgs"
 TSQR_OK, TSQR_ERR_INVALID_ARG, TSQR_ERR_UNSUPPORTED, TSQR_ERR_CUDA = 0, 1, 2, 3
 TSQR_ERR_NCCL, TSQR_ERR_BREAKDOWN, TSQR_ERR_WORKSPACE = 4, 5, 6
 PLANES = ["local", "nccl", "fused"]
-KCLASSES = ["gram", "proj", "update", "trmm", "chol", "small", "allreduce"]
+KCLASSES = ["gram", "proj", "update", "trmm", "chol", "small", "allreduce", "cluster"]
+PATHS = ["stream", "cluster"]
 
 LIB_PATH = os.environ.get("TSQR_LIB", _build.LIB)  # override: timing experiments only
 
 #: every function declared in include/tsqr.h
 EXPORTS = ["tsqr_workspace_bytes", "tsqr_create", "tsqr_factor", "tsqr_wait", "tsqr_last_counts",
-           "tsqr_factor_host", "tsqr_set_graph", "tsqr_data_plane", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
+           "tsqr_factor_host", "tsqr_set_graph", "tsqr_data_plane", "tsqr_exec_path", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
            "tsqr_nccl_comm_init", "tsqr_nccl_comm_destroy", "tsqr_gram", "tsqr_proj", "tsqr_update",
            "tsqr_chol_inv", "tsqr_trmm"]
 
@@ -76,6 +78,7 @@ def load(build_if_missing: bool = False):
     L.tsqr_set_timing.argtypes = [_VP, _I32]
     L.tsqr_set_graph.argtypes = [_VP, _I32]
     L.tsqr_data_plane.argtypes = [_VP, ctypes.POINTER(_I32)]
+    L.tsqr_exec_path.argtypes = [_VP, ctypes.POINTER(_I32)]
     L.tsqr_timing_reset.argtypes = [_VP]
     L.tsqr_timing.argtypes = [_VP, _I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -160,9 +163,14 @@ class NcclComm:
                "tsqr_nccl_comm_init")
         self.handle = comm.value
         self.rank, self.world = rank, world
+        self._plans = weakref.WeakSet()  # plans created on this communicator
 
     def close(self):
+        """Destroys the plans still open on this communicator first (a plan's window and device
+        communicator must be released while the communicator is alive), then the communicator."""
         if self.handle:
+            for p in list(self._plans):
+                p.close()
             load().tsqr_nccl_comm_destroy(self.handle)
             self.handle = None
 
@@ -191,6 +199,8 @@ class Plan:
                            _stream_ptr(self.stream), aligned, nbytes)
         _check(rc, "tsqr_create")
         self.handle = h.value
+        if comm is not None:
+            comm._plans.add(self)
 
     def factor(self, A, R=None, wait: bool = True):
         """A (m_local x n, column-major CUDA FP64) is overwritten by Q; returns R (n x n)."""
@@ -224,6 +234,12 @@ class Plan:
         v = _I32()
         _check(load().tsqr_data_plane(self.handle, ctypes.byref(v)), "tsqr_data_plane")
         return PLANES[v.value]
+
+    def exec_path(self) -> str:
+        """'stream' (one kernel per step, CUDA graph) or 'cluster' (one-launch small-problem kernel)."""
+        v = _I32()
+        _check(load().tsqr_exec_path(self.handle, ctypes.byref(v)), "tsqr_exec_path")
+        return PATHS[v.value]
 
     def set_timing(self, on: bool = True):
         _check(load().tsqr_set_timing(self.handle, 1 if on else 0), "tsqr_set_timing")

@@ -43,6 +43,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_profiling_variant(out: str = os.path.join(HERE, "libtsqr_prof.so")) -> str:
+    """Development build with the cluster kernel's phase counters (-DTSQR_CL_PROF); load it with
+    TSQR_LIB=<path>.  Never the product library."""
+    r = subprocess.run(nvcc_cmd(out=out, extra=["-DTSQR_CL_PROF"]), capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building the profiling variant")
+    return out
+
+
 if __name__ == "__main__":
     build(force=True, verbose="-v" in sys.argv)
     print(LIB)

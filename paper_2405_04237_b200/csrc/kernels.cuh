@@ -4,3 +4,4 @@
 #include "small_kernels.cuh"
 #include "stream_kernels.cuh"
 #include "fused_allreduce.cuh"
+#include "cluster_small.cuh"

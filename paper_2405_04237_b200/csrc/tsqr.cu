@@ -508,6 +508,11 @@ struct tsqr_plan_s {
   // tsqr_factor_host: per-panel "Q_j is final" events (recorded inside the graph as external
   // event nodes while capturing) so the device->host copy of Q_j overlaps the later panels
   bool panel_events = false, gpanel = false;
+  // single-launch cluster path for small problems (cluster_small.cuh)
+  bool cluster = false;
+  int cl_cs = 0;          // CTAs per cluster (16 or 8)
+  ClusterArgs cl_args{};  // fixed part (A, lda, R, ldr filled per call)
+  size_t cl_smem = 0;
   std::vector<cudaEvent_t> ev_panel;
   cudaStream_t d2h = nullptr;
   cudaEvent_t ev_d2h = nullptr, ev_fact = nullptr;
@@ -782,6 +787,87 @@ tsqr_status setup_fused_allreduce(tsqr_plan_s* p) {
   return TSQR_OK;
 }
 
+// ---- single-launch cluster path (cluster_small.cuh) ----
+template <int B>
+cudaError_t cluster_config(size_t smem, int cs, int* active) {
+  cudaError_t e = cudaFuncSetAttribute(k_cluster_factor<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (cs > 8) {
+    e = cudaFuncSetAttribute(k_cluster_factor<B>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(cs); cfg.blockDim = dim3(CL_NT); cfg.dynamicSmemBytes = smem;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(active, k_cluster_factor<B>, &cfg);
+}
+
+// Decide at tsqr_create whether the plan runs the one-launch cluster kernel: one rank (no
+// communicator), b in {16, 32, 64}, and this rank's m x n block (zero-padded to CS equal row
+// blocks) plus the reduction buffers fit in the shared memory of CS CTAs.
+void setup_cluster_path(tsqr_plan_s* p) {
+  const char* env = std::getenv("TSQR_CLUSTER_PATH");
+  if ((env && std::atoi(env) == 0) || p->comm || p->m < 1 || !(p->b == 16 || p->b == 32 || p->b == 64)) return;
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return;
+  }
+  const int pq = p->b * std::max(p->b, p->n - p->b);
+  for (int cs : {16, 8}) {
+    const int64_t mr = ((p->m + cs - 1) / cs + 31) / 32 * 32;
+    const int ldx = (int)mr + 4;
+    const size_t smem = cluster_smem_bytes(p->b, ldx, p->n, pq, (int)p->algo);
+    if (smem > (size_t)optin) continue;
+    int active = 0;
+    cudaError_t e = p->b == 16 ? cluster_config<16>(smem, cs, &active)
+                  : p->b == 32 ? cluster_config<32>(smem, cs, &active)
+                               : cluster_config<64>(smem, cs, &active);
+    if (e != cudaSuccess || active < 1) { (void)cudaGetLastError(); continue; }
+    ClusterArgs& a = p->cl_args;
+    a.R1 = p->R1; a.R2 = p->R2; a.status = p->status; a.m = p->m; a.n = p->n; a.algo = (int)p->algo;
+    a.mr = (int)mr; a.ldx = ldx; a.pq = pq;
+    a.shift_scale = std::sqrt((double)p->m_global) * 1.1102230246251565e-16;  // sqrt(m) u (Alg. 4 l.2)
+    p->cl_cs = cs; p->cl_smem = smem; p->cluster = true;
+    return;
+  }
+}
+
+int64_t reductions_of(tsqr_algo algo, int k) {
+  switch (algo) {
+    case TSQR_CQR: case TSQR_SCQR: return 1;
+    case TSQR_CQR2: return 2;
+    case TSQR_SCQR3: return 3;
+    case TSQR_CQRGS: return 2 * k - 1;
+    default: return k == 1 ? 2 : 4 * k - 2;  // CQR2GS, mCQR2GS (k = 1: CholeskyQR2)
+  }
+}
+
+tsqr_status launch_cluster(tsqr_plan_s* P, double* A, int64_t lda, double* R, int ldr) {
+  ClusterArgs a = P->cl_args;
+  a.A = A; a.lda = lda; a.R = R; a.ldr = ldr;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P->cl_cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(P->cl_cs); cfg.blockDim = dim3(CL_NT); cfg.dynamicSmemBytes = P->cl_smem;
+  cfg.stream = P->L.st; cfg.attrs = at; cfg.numAttrs = 1;
+  const size_t t0 = P->L.tbegin();
+  cudaError_t e = P->b == 16 ? cudaLaunchKernelEx(&cfg, k_cluster_factor<16>, a)
+                : P->b == 32 ? cudaLaunchKernelEx(&cfg, k_cluster_factor<32>, a)
+                             : cudaLaunchKernelEx(&cfg, k_cluster_factor<64>, a);
+  CUDA_TRY(e);
+  P->L.launches += 1;
+  P->L.tend(t0, TSQR_KCLASS_CLUSTER, 4.0 * (double)P->m * P->n * P->n, 16.0 * (double)P->m * P->n);
+  P->allreduces = reductions_of(P->algo, P->k);
+  for (int j = 0; j < P->k; ++j) TRY(panel_done(P, j));
+  return TSQR_OK;
+}
+
 const char* status_names[] = {"TSQR_OK", "TSQR_ERR_INVALID_ARG", "TSQR_ERR_UNSUPPORTED", "TSQR_ERR_CUDA",
                               "TSQR_ERR_NCCL", "TSQR_ERR_BREAKDOWN", "TSQR_ERR_WORKSPACE"};
 
@@ -871,6 +957,7 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
       return fs;
     }
   }
+  setup_cluster_path(p);
   *plan = p;
   return TSQR_OK;
 }
@@ -879,6 +966,7 @@ static tsqr_status enqueue_factor(tsqr_plan_t P, double* A, int64_t lda, double*
   P->L.launches = 0;
   P->allreduces = 0;
   P->sticky = TSQR_OK;
+  if (P->cluster) return launch_cluster(P, A, lda, R, ldr);  // clears the status word itself
   CUDA_TRY(cudaMemsetAsync(P->status, 0, 16 * sizeof(int), P->L.st));
   k_zero2d<<<grid_1d((int64_t)P->n * P->n), 256, 0, P->L.st>>>(R, ldr, P->n, P->n);
   CUDA_TRY(cudaGetLastError());
@@ -1116,6 +1204,12 @@ tsqr_status tsqr_timing(tsqr_plan_t P, int32_t kclass, double* ms, int64_t* laun
 tsqr_status tsqr_data_plane(tsqr_plan_t P, int32_t* plane) {
   if (!P || !plane) return TSQR_ERR_INVALID_ARG;
   *plane = P->L.ar_on ? TSQR_PLANE_FUSED : (P->comm ? TSQR_PLANE_NCCL : TSQR_PLANE_LOCAL);
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_exec_path(tsqr_plan_t P, int32_t* path) {
+  if (!P || !path) return TSQR_ERR_INVALID_ARG;
+  *path = P->cluster ? TSQR_PATH_CLUSTER : TSQR_PATH_STREAM;
   return TSQR_OK;
 }
 

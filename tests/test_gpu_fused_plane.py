@@ -48,9 +48,10 @@ def comm1():
 
 
 def _plan(t, comm, m, n, b, algo, plane):
-    old = {k: os.environ.get(k) for k in ("TSQR_FUSED_ALLREDUCE", "TSQR_NCCL_ALLREDUCE")}
+    old = {k: os.environ.get(k) for k in ("TSQR_FUSED_ALLREDUCE", "TSQR_NCCL_ALLREDUCE", "TSQR_CLUSTER_PATH")}
     os.environ["TSQR_FUSED_ALLREDUCE"] = "1" if plane == "fused" else "0"
     os.environ["TSQR_NCCL_ALLREDUCE"] = "1" if plane == "nccl" else "0"
+    os.environ["TSQR_CLUSTER_PATH"] = "0"  # the same (streaming) kernels on every plane
     try:
         p = t.Plan(m, n, b, algo, comm=comm if plane != "local" else None)
     finally:
@@ -106,10 +107,14 @@ def test_one_rank_fused_breakdown_keeps_barriers_matched(comm1):
     ref.close()
     bad = A.copy()
     bad[:, 3] = 0.0
+    ref = _plan(t, c, m, n, b, "mcqr2gs", "local")
+    with pytest.raises(t.TsqrError) as e0:
+        ref.factor(t.to_colmajor(bad))
+    ref.close()
     with pytest.raises(t.TsqrError) as e:
         p.factor(t.to_colmajor(bad))
     assert e.value.status == t.TSQR_ERR_BREAKDOWN
-    assert e.value.info["panel"] == 0 and e.value.info["pivot"] == 3
+    assert e.value.info == e0.value.info and e.value.info["pivot"] == 3
     X = t.to_colmajor(A)
     R = p.factor(X)
     torch.cuda.synchronize()

@@ -26,14 +26,31 @@ def T():
     return t
 
 
-def run_gpu(T, A, b, algo):
+def run_gpu(T, A, b, algo, path=None):
+    """path: None (the plan's choice), 'stream' or 'cluster' (asserted)."""
+    import os
     Ad = T.to_colmajor(A)
+    old = os.environ.get("TSQR_CLUSTER_PATH")
+    if path == "stream":
+        os.environ["TSQR_CLUSTER_PATH"] = "0"
     try:
-        R = T.factor(Ad, b, algo)
+        p = T.Plan(A.shape[0], A.shape[1], b, algo)
+    finally:
+        if path == "stream":
+            if old is None:
+                os.environ.pop("TSQR_CLUSTER_PATH")
+            else:
+                os.environ["TSQR_CLUSTER_PATH"] = old
+    if path is not None:
+        assert p.exec_path() == path
+    try:
+        R = p.factor(Ad)
     except T.TsqrError as e:
         if e.status == T.TSQR_ERR_BREAKDOWN:
             return None, None, e.info
         raise
+    finally:
+        p.close()
     return Ad.cpu().numpy(), R.cpu().numpy(), None
 
 
@@ -46,12 +63,15 @@ def check_invariants(R):
     assert np.all(np.diag(R) > 0)
 
 
+@pytest.mark.parametrize("path", ["cluster", "stream"])
 @pytest.mark.parametrize("kappa", KAPPAS)
-def test_cfg1_mcqr2gs_sweep(T, orc, kappa):
-    """BASELINE configs[0]: m=4096, n=64, b=16, mCQR2GS, kappa sweep 1e2..1e15."""
+def test_cfg1_mcqr2gs_sweep(T, orc, kappa, path):
+    """BASELINE configs[0]: m=4096, n=64, b=16, mCQR2GS, kappa sweep 1e2..1e15, on both
+    execution paths (the one-launch cluster kernel the plan picks at this size, and the
+    streaming kernels)."""
     A, _, _ = synth.generate_np(4096, 64, kappa, seed=0)
     Qo, Ro, io = orc.factor(A, 16, "mcqr2gs")
-    Q, R, info = run_gpu(T, A, 16, "mcqr2gs")
+    Q, R, info = run_gpu(T, A, 16, "mcqr2gs", path)
     assert io["status"] == 0 and info is None
     check_invariants(R)
     orth, res = gates(orc, A, Q, R)
@@ -62,11 +82,12 @@ def test_cfg1_mcqr2gs_sweep(T, orc, kappa):
         assert np.linalg.norm(Q - Qo) / np.linalg.norm(Qo) <= 1e-11
 
 
+@pytest.mark.parametrize("path", ["cluster", "stream"])
 @pytest.mark.parametrize("seed", [1, 2, 3, 4])
-def test_cfg1_seeds(T, orc, seed):
+def test_cfg1_seeds(T, orc, seed, path):
     A, _, _ = synth.generate_np(4096, 64, 1e8, seed=seed)
     Qo, Ro, _ = orc.factor(A, 16, "mcqr2gs")
-    Q, R, info = run_gpu(T, A, 16, "mcqr2gs")
+    Q, R, info = run_gpu(T, A, 16, "mcqr2gs", path)
     assert info is None
     assert np.linalg.norm(R - Ro) / np.linalg.norm(Ro) <= 1e-10
     orth, res = gates(orc, A, Q, R)
@@ -92,12 +113,13 @@ def same_class(o_orc, o_gpu):
     return {co, cg} == {"fail", "breakdown"}
 
 
+@pytest.mark.parametrize("path", ["cluster", "stream"])
 @pytest.mark.parametrize("algo,b", [("cqr2gs", 16), ("cqr2", 64), ("cqr2gs", 32)])
 @pytest.mark.parametrize("kappa", [1e2, 1e5, 1e8, 1e10, 1e12, 1e15])
-def test_cfg1_other_algorithms_outcome(T, orc, algo, b, kappa):
+def test_cfg1_other_algorithms_outcome(T, orc, algo, b, kappa, path):
     A, _, _ = synth.generate_np(4096, 64, kappa, seed=0)
     Qo, Ro, io = orc.factor(A, b, algo)
-    Q, R, info = run_gpu(T, A, b, algo)
+    Q, R, info = run_gpu(T, A, b, algo, path)
     oo, og = _outcome(orc, A, Qo, Ro), _outcome(orc, A, Q, R)
     if kappa <= 1e8:
         assert oo[0] == og[0] == "pass"
@@ -413,10 +435,10 @@ def test_maximum_width_n4096(T):
     check_invariants(R.cpu().numpy())
     p.close()
     torch.cuda.synchronize()
-    # ||Q^TQ - I||_F grows like n * (per-entry error): the BJ gate (1e-13 at n = 512) is held at
-    # the same per-entry level through the paper's normalisation (R-1): / sqrt(n)
+    # measured 5.5e-14 un-normalised (error-free verifier): the BJ gate holds without R-1's
+    # normalisation even at n = 4096
     print(f"n=4096: ||Q^TQ-I||_F = {orth:.3e} (un-normalised), /sqrt(n) = {orth / math.sqrt(n):.3e}")
-    assert orth / math.sqrt(n) <= 1e-13 / math.sqrt(512) and res <= 1e-14, (orth, res)
+    assert orth <= 1e-13 and res <= 1e-14, (orth, res)
 
 
 def test_verifier_on_gpu_equals_oracle_metrics(T, orc):
@@ -458,8 +480,8 @@ def test_r_parity_many_panels(T, orc, m, n, b, kappa):
 @pytest.mark.parametrize("b", [128, 256])
 def test_full_size_cfg4_in_bench_configuration(T, orc, b):
     """BASELINE configs[3] at full size (2^20 x 2048, kappa = 1e12, b = 128 / 256: 16 / 8 panels,
-    blocked Cholesky + TRMM) in the bench's graph-replay configuration: gates (n = 2048 > 512:
-    the per-entry level of R-1) and invariants, R_11 vs the oracle's CQR2 of the first panel."""
+    blocked Cholesky + TRMM) in the bench's graph-replay configuration: the un-normalised gates
+    and invariants, R_11 vs the oracle's CQR2 of the first panel."""
     import torch
     from harness import verify
     m, n = 1 << 20, 2048
@@ -481,7 +503,8 @@ def test_full_size_cfg4_in_bench_configuration(T, orc, b):
     torch.cuda.empty_cache()
     check_invariants(Rh)
     print(f"cfg4 b={b}: ||Q^TQ-I||_F = {orth:.3e} (/sqrt(n) {orth / math.sqrt(n):.3e}), residual {res:.3e}")
-    assert orth / math.sqrt(n) <= 1e-13 / math.sqrt(512) and res <= 1e-14, (orth, res)
+    # measured 1.9e-14 (b = 128) / 3.7e-14 (b = 256): the un-normalised BJ gate holds at n = 2048
+    assert orth <= 1e-13 and res <= 1e-14, (orth, res)
     _, R11, info = orc.factor(A1, b, "cqr2")
     assert info["status"] == 0
     assert np.linalg.norm(Rh[:b, :b] - R11) / np.linalg.norm(R11) <= 1e-10
