@@ -109,12 +109,18 @@ def local_gram(Q, chunk: int = CHUNK, m_global: int | None = None, dd: bool = Fa
     return (acc.hi, acc.lo) if dd else acc.value()
 
 
+def _comm_device(group, dev):
+    """Tensors passed to torch.distributed collectives live where the group's backend wants them."""
+    import torch.distributed as dist
+    return dev if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+
 def orthogonality(Q, group=None, chunk: int = CHUNK) -> float:
     """||Q^T Q - I||_F (un-normalised; divide by sqrt(n) for P:104's form)."""
     m = Q.shape[0]
     if group is not None:
         import torch.distributed as dist
-        mt = torch.tensor([float(m)], dtype=torch.float64)
+        mt = torch.tensor([float(m)], dtype=torch.float64, device=_comm_device(group, Q.device))
         dist.all_reduce(mt, group=group)
         m = int(mt.item())
     n = Q.shape[1]
@@ -126,11 +132,12 @@ def orthogonality(Q, group=None, chunk: int = CHUNK) -> float:
     else:  # the rank shares are O(sqrt(m_r)/m), not small: gather them unrounded, sum in rank order
         import torch.distributed as dist
         w = dist.get_world_size(group)
-        his = [torch.empty((n, n), dtype=torch.float64) for _ in range(w)]
-        los = [torch.empty((n, n), dtype=torch.float64) for _ in range(w)]
-        dist.all_gather(his, hi.cpu().contiguous(), group=group)
-        dist.all_gather(los, lo.cpu().contiguous(), group=group)
-        acc = _DD(torch.zeros((n, n), dtype=torch.float64))
+        cd = _comm_device(group, Q.device)
+        his = [torch.empty((n, n), dtype=torch.float64, device=cd) for _ in range(w)]
+        los = [torch.empty((n, n), dtype=torch.float64, device=cd) for _ in range(w)]
+        dist.all_gather(his, hi.to(cd).contiguous(), group=group)
+        dist.all_gather(los, lo.to(cd).contiguous(), group=group)
+        acc = _DD(torch.zeros((n, n), dtype=torch.float64, device=cd))
         for h, l in zip(his, los):
             acc.add(h)
             acc.add(l)
@@ -155,8 +162,10 @@ def residual(A0, Q, R, group=None, chunk: int = RCHUNK) -> float:
         d = acc.value()
         num = num + (d * d).sum()
         den = den + (a * a).sum()
-    v = torch.stack([num, den]).cpu()
+    v = torch.stack([num, den])
     if group is not None:
         import torch.distributed as dist
+        v = v.to(_comm_device(group, A0.device))
         dist.all_reduce(v, group=group)
+    v = v.cpu()
     return math.sqrt(float(v[0]) / float(v[1])) if float(v[1]) > 0 else 0.0

@@ -18,6 +18,13 @@
  *                 W = A^T A + s I, s = sqrt(m) u ||A||_F^2, m the global row count,
  *                 u = 2^-53) followed by CQR2; R = R2 R1.  b == n.  3 allreduces.
  *   TSQR_SCQR     single shifted CholeskyQR pass (Alg. 4)           -- tests
+ *   TSQR_MCQR2GS_ADAPTIVE  mCQR2GS with the runtime decision on the number of CholeskyQR
+ *                 repetitions the paper proposes (DESIGN R-23): after a
+ *                 panel's first CholeskyQR (U1, Z = U1^{-1}) the estimate
+ *                 E = max(u nu(U1)^2 nu(Z)^2, u nu(R_{1:j,j}) nu(Z)), nu(M) = ||M||_F/sqrt(b),
+ *                 decides on the device (identically on every rank) whether the repetition
+ *                 (l.7-8; the second CQR of l.1) is skipped: E <= tau (tsqr_set_adapt_tau,
+ *                 default 2^-50) -> R_jj = U1.  tau = 0: bitwise TSQR_MCQR2GS
  *
  * Conventions for every entry point:
  *   - Matrices are FP64, COLUMN-MAJOR: element (r, c) of X is X[r + c*ldX].
@@ -68,7 +75,8 @@ typedef enum {
   TSQR_CQR = 3,
   TSQR_CQRGS = 4,
   TSQR_SCQR3 = 5,
-  TSQR_SCQR = 6
+  TSQR_SCQR = 6,
+  TSQR_MCQR2GS_ADAPTIVE = 7
 } tsqr_algo;
 
 /* Where a Cholesky breakdown happened (identical on every rank, since every rank
@@ -177,6 +185,13 @@ tsqr_status tsqr_timing(tsqr_plan_t plan, int32_t kclass, double* ms, int64_t* l
  * that later calls with the same A, lda, R, ldr and timing setting replay with one launch.
  * enable = 0 switches to eager enqueueing. */
 tsqr_status tsqr_set_graph(tsqr_plan_t plan, int32_t enable);
+
+/* TSQR_MCQR2GS_ADAPTIVE: threshold tau of the skip rule (default 2^-50 ~ 8.9e-16; 0 never
+ * skips).  Takes effect at the next tsqr_factor (it re-captures the CUDA graph). */
+tsqr_status tsqr_set_adapt_tau(tsqr_plan_t plan, double tau);
+/* Panels whose CholeskyQR repetition the last factorisation skipped (valid after tsqr_wait;
+ * 0 for the other algorithms). */
+tsqr_status tsqr_skipped_panels(tsqr_plan_t plan, int32_t* panels);
 
 /* Which cross-GPU data plane the plan's allreduces use: TSQR_PLANE_LOCAL (no communicator,
  * no exchange), TSQR_PLANE_NCCL (k_reduce + ncclAllReduce) or TSQR_PLANE_FUSED (the split-row

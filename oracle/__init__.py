@@ -19,9 +19,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CQR2, CQR2GS, MCQR2GS, CQR, CQRGS, SCQR3, SCQR = 0, 1, 2, 3, 4, 5, 6
+CQR2, CQR2GS, MCQR2GS, CQR, CQRGS, SCQR3, SCQR, MCQR2GS_ADAPTIVE = 0, 1, 2, 3, 4, 5, 6, 7
 ALGOS = {"cqr2": CQR2, "cqr2gs": CQR2GS, "mcqr2gs": MCQR2GS, "cqr": CQR, "cqrgs": CQRGS, "scqr3": SCQR3,
-         "scqr": SCQR}
+         "scqr": SCQR, "mcqr2gs_adaptive": MCQR2GS_ADAPTIVE}
 OK, ERR_ARG, ERR_BREAKDOWN, ERR_NOMEM = 0, 1, 5, 6
 
 BUILD_CMD = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
@@ -56,6 +56,13 @@ def lib():
         _lib = ctypes.CDLL(build())
         L = _lib
         L.orc_set_threads.argtypes = [ctypes.c_int]
+        L.orc_set_adapt_tau.argtypes = [ctypes.c_double]
+        L.orc_get_adapt_tau.restype = ctypes.c_double
+        L.orc_adapt_skipped.restype = ctypes.c_int64
+        L.orc_diag_ratio.argtypes = [_P, _I64, _I64]
+        L.orc_diag_ratio.restype = ctypes.c_double
+        L.orc_kappa_f.argtypes = [_P, _I64, _I64]
+        L.orc_kappa_f.restype = ctypes.c_double
         L.orc_get_threads.restype = ctypes.c_int
         L.orc_gram.argtypes = [_P, _I64, _I64, _I64, _P, _I64]
         L.orc_atb.argtypes = [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64]
@@ -225,6 +232,31 @@ def mcqr2gs_panel(Qprev, P, R_col=None):
     if rc != OK:
         return None, None, None, d
     return X[:, c0:], R[:c0, c0:].copy(), R[c0:, c0:].copy(), d
+
+
+def set_adapt_tau(tau: float) -> None:
+    """Threshold of the adaptive repetition rule (NEXT-f4, oracle.c mcqr2gs_adaptive)."""
+    lib().orc_set_adapt_tau(float(tau))
+
+
+def get_adapt_tau() -> float:
+    return float(lib().orc_get_adapt_tau())
+
+
+def adapt_skipped() -> int:
+    """Panels whose CholeskyQR repetition the last adaptive factorisation skipped."""
+    return int(lib().orc_adapt_skipped())
+
+
+def diag_ratio(U) -> float:
+    U = _f(U)
+    return float(lib().orc_diag_ratio(_p(U), U.shape[0], U.shape[0]))
+
+
+def kappa_f(U) -> float:
+    """||U||_F ||U^{-1}||_F of an upper-triangular U (the adaptive rule's estimate)."""
+    U = _f(U)
+    return float(lib().orc_kappa_f(_p(U), U.shape[0], U.shape[0]))
 
 
 def householder(A):

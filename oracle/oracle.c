@@ -48,6 +48,7 @@
 #define ORC_CQRGS 4
 #define ORC_SCQR3 5
 #define ORC_SCQR 6
+#define ORC_MCQR2GS_ADAPTIVE 7
 
 /* unit roundoff of FP64 round-to-nearest-even: u = 2^-53 */
 #define ORC_UNIT_ROUNDOFF 1.1102230246251565e-16
@@ -66,6 +67,14 @@ static int g_threads = 1;
 /* number of Sigma_rows reductions performed: each is one Allreduce of the
  * distributed algorithm (Alg. 2 l.4 P:154; Alg. 7 l.3, l.8 P:345) */
 static int64_t g_reductions = 0;
+
+/* NEXT-f4: threshold tau of the adaptive repetition rule (mcqr2gs_adaptive below) and
+ * the number of panels whose repetition the last adaptive factorisation skipped */
+static double g_adapt_tau = 8.8817841970012523e-16; /* 2^-50 (R-23) */
+static int64_t g_adapt_skipped = 0;
+void orc_set_adapt_tau(double tau) { g_adapt_tau = tau; }
+double orc_get_adapt_tau(void) { return g_adapt_tau; }
+int64_t orc_adapt_skipped(void) { return g_adapt_skipped; }
 
 void orc_set_threads(int t) { g_threads = t > 0 ? t : 1; }
 int orc_get_threads(void) { return g_threads; }
@@ -467,6 +476,121 @@ static int mcqr2gs(double* X, int64_t ldx, int64_t m, int64_t n, int64_t b, doub
   return rc;
 }
 
+/* Cholesky diagonal ratio rho = max_i U_ii / min_i U_ii of an upper-triangular U with positive
+ * diagonal: a LOWER bound of kappa_2(U) (U_ii are the norms of the panel's columns after
+ * orthogonalisation against the previous ones), SURVEY NEXT-f4's suggested indicator. */
+double orc_diag_ratio(const double* U, int64_t ldu, int64_t b) {
+  double mx = U[0], mn = U[0];
+  for (int64_t i = 1; i < b; ++i) {
+    const double d = U[i + i * ldu];
+    if (d > mx) mx = d;
+    if (d < mn) mn = d;
+  }
+  return mx / mn;
+}
+
+/* Frobenius condition estimate kappa_F(U) = ||U||_F ||U^{-1}||_F of an upper-triangular U:
+ * an UPPER bound of kappa_2(U) (within a factor b of it), from the explicit inverse
+ * (orc_tri_inv) -- the quantity the adaptive rule uses (R-23). */
+double orc_kappa_f(const double* U, int64_t ldu, int64_t b) {
+  double* Z = (double*)malloc(sizeof(double) * (size_t)(b * b));
+  if (!Z) return INFINITY;
+  orc_tri_inv(U, ldu, b, Z, b);
+  double su = 0.0, sz = 0.0;
+  for (int64_t j = 0; j < b; ++j)
+    for (int64_t i = 0; i <= j; ++i) {
+      su += U[i + j * ldu] * U[i + j * ldu];
+      sz += Z[i + j * b] * Z[i + j * b];
+    }
+  free(Z);
+  return sqrt(su) * sqrt(sz);
+}
+
+/* The adaptive rule's estimate of the loss of orthogonality one CholeskyQR leaves on panel j
+ * (R-23): with Z = U1^{-1} (orc_tri_inv),
+ *   own    = u nu(U1)^2 nu(Z)^2            (u kappa(V)^2)
+ *   across = u nu(R_{1:j,j}) nu(Z)         (the projection of l.3-4 leaves ~u ||A_j|| along the
+ *                                           earlier panels, A_j = Q R_{1:j,j}; the CQR scales it
+ *                                           by U1^{-1}: CQRGS's loss of orthogonality)
+ * with nu(M) = ||M||_F / sqrt(b), the RMS singular value (1 for an orthonormal panel).
+ * E_j = max(own, across).  Rcol points at R_{1,j} (rows 0..c0-1 hold R_{1:j-1,j} = the line-5
+ * projections Y of the earlier steps), leading dimension ldr. */
+double orc_adapt_estimate(const double* U1, int64_t b, const double* Rcol, int64_t ldr, int64_t c0) {
+  double* Z = (double*)malloc(sizeof(double) * (size_t)(b * b));
+  if (!Z) return INFINITY;
+  orc_tri_inv(U1, b, b, Z, b);
+  double su = 0.0, sz = 0.0, sy = 0.0;
+  for (int64_t j = 0; j < b; ++j) {
+    for (int64_t i = 0; i <= j; ++i) {
+      su += U1[i + j * b] * U1[i + j * b];
+      sz += Z[i + j * b] * Z[i + j * b];
+    }
+    for (int64_t i = 0; i < c0; ++i) sy += Rcol[i + j * ldr] * Rcol[i + j * ldr];
+  }
+  free(Z);
+  /* RMS singular values nu(M) = ||M||_F / sqrt(b): 1 for an orthonormal panel, whatever b */
+  const double bb = (double)b;
+  const double own = ORC_UNIT_ROUNDOFF * (su / bb) * (sz / bb);
+  const double across = ORC_UNIT_ROUNDOFF * sqrt((sy + su) / bb) * sqrt(sz / bb);
+  return own > across ? own : across;
+}
+
+/* Adaptive mCQR2GS ("the condition number steeply decreases as we
+ * proceed with the panel processing, opening up a space for further optimisation in reducing
+ * the number of flops by applying a runtime decision on how many repetitions of CholeskyQR to
+ * perform"; reading R-23).  Alg. 8 with one decision per panel, taken after the panel's FIRST
+ * CholeskyQR (U1 = chol(W1), W1 the allreduced Gram -- identical on every rank):
+ *     rho_j = orc_diag_ratio(U1)
+ *     rho_j <= tau:  the repetition is skipped -- panel 1: no second CQR of l.1, R_11 = U1;
+ *                    panel j >= 2: lines 7-8 skipped, R_jj = U1 (R_{1:j-1,j} keeps Y);
+ *     otherwise:     Alg. 8 unchanged (second CQR; l.7-8 and R-8 bookkeeping).
+ * One CholeskyQR leaves ||Q^T Q - I|| ~ u kappa(panel)^2, so tau bounds the
+ * estimated loss by ~u tau^2.  tau = 0 never skips: bitwise mCQR2GS.  tau = +inf always
+ * skips: bitwise CQRGS (Alg. 7), whose per-panel steps are then the same operations in the same
+ * order.  Panels skipped: orc_adapt_skipped(). */
+static int mcqr2gs_adaptive(double* X, int64_t ldx, int64_t m, int64_t n, int64_t b, double* R, int64_t ldr,
+                            orc_info* info) {
+  int64_t k = (n + b - 1) / b;
+  g_adapt_skipped = 0;
+  double* U1 = (double*)malloc(sizeof(double) * (size_t)(b * b));
+  double* U2 = (double*)malloc(sizeof(double) * (size_t)(b * b));
+  double* C = (double*)malloc(sizeof(double) * (size_t)(n * b));
+  int rc = ORC_OK;
+  if (!U1 || !U2 || !C) { rc = fail(info, ORC_ERR_NOMEM, 0, 0, 0); goto done; }
+  for (int64_t j = 0; j < k; ++j) {
+    int64_t c0 = j * b, bj = (c0 + b <= n) ? b : n - c0;
+    double* Xj = X + c0 * ldx;
+    if (j > 0) { /* l.3-5 */
+      int64_t cp = c0 - b;
+      double* Y = R + cp + c0 * ldr;
+      rc = orc_atb(X + cp * ldx, ldx, Xj, ldx, m, b, n - c0, Y, ldr);
+      if (rc != ORC_OK) goto done;
+      orc_sub_prod(Xj, ldx, X + cp * ldx, ldx, Y, ldr, m, b, n - c0);
+    }
+    /* first CQR: l.1 (first half) / l.6 */
+    rc = cqr(Xj, ldx, m, bj, U1, bj, info);
+    if (rc != ORC_OK) { rc = fail(info, rc, 1, (int)j + 1, 1); goto done; }
+    if (orc_adapt_estimate(U1, bj, R + c0 * ldr, ldr, c0) <= g_adapt_tau) { /* skipped: R_jj = U1 */
+      ++g_adapt_skipped;
+      for (int64_t jj = 0; jj < bj; ++jj)
+        for (int64_t ii = 0; ii <= jj; ++ii) R[c0 + ii + (c0 + jj) * ldr] = U1[ii + jj * bj];
+      continue;
+    }
+    if (c0 > 0) { /* l.7 */
+      rc = orc_atb(X, ldx, Xj, ldx, m, c0, bj, C, c0);
+      if (rc != ORC_OK) goto done;
+      orc_sub_prod(Xj, ldx, X, ldx, C, c0, m, c0, bj);
+    }
+    rc = cqr(Xj, ldx, m, bj, U2, bj, info); /* second CQR: l.1 (second half) / l.8 */
+    if (rc != ORC_OK) { rc = fail(info, rc, 1, (int)j + 1, 2); goto done; }
+    orc_matmul(U2, bj, U1, bj, bj, bj, bj, R + c0 + c0 * ldr, ldr, 1, 0);   /* R_jj = U2 U1 */
+    if (c0 > 0) orc_matmul(C, c0, U1, bj, c0, bj, bj, R + c0 * ldr, ldr, 0, 1); /* R-8 */
+  }
+done:
+  free(U1); free(U2); free(C);
+  return rc;
+}
+
 /* Top-level factorisation.  A (m x n, lda >= m) is overwritten with Q; R (n x n,
  * ldr >= n) receives the upper-triangular factor with exact zeros below the
  * diagonal.  b is the panel width (ignored for CQR / CQR2).  Returns ORC_OK,
@@ -475,7 +599,8 @@ int orc_factor(double* A, int64_t lda, int64_t m, int64_t n, int64_t b, int algo
                int64_t ldr, orc_info* info) {
   if (info) memset(info, 0, sizeof(*info));
   if (!A || !R || m < n || n < 1 || lda < m || ldr < n) return fail(info, ORC_ERR_ARG, 0, 0, 0);
-  if ((algo == ORC_CQR2GS || algo == ORC_MCQR2GS || algo == ORC_CQRGS) && (b < 1 || b > n))
+  if ((algo == ORC_CQR2GS || algo == ORC_MCQR2GS || algo == ORC_CQRGS || algo == ORC_MCQR2GS_ADAPTIVE) &&
+      (b < 1 || b > n))
     return fail(info, ORC_ERR_ARG, 0, 0, 0);
   zero_mat(R, ldr, n, n);
   int rc = ORC_OK;
@@ -504,6 +629,9 @@ int orc_factor(double* A, int64_t lda, int64_t m, int64_t n, int64_t b, int algo
     }
     case ORC_MCQR2GS:
       rc = mcqr2gs(A, lda, m, n, b, R, ldr, info);
+      break;
+    case ORC_MCQR2GS_ADAPTIVE:
+      rc = mcqr2gs_adaptive(A, lda, m, n, b, R, ldr, info);
       break;
     case ORC_SCQR: {
       rc = scqr(A, lda, m, n, R, ldr, info, ORC_UNIT_ROUNDOFF);

@@ -18,9 +18,9 @@ import weakref
 
 from . import build as _build
 
-CQR2, CQR2GS, MCQR2GS, CQR, CQRGS, SCQR3, SCQR = 0, 1, 2, 3, 4, 5, 6
+CQR2, CQR2GS, MCQR2GS, CQR, CQRGS, SCQR3, SCQR, MCQR2GS_ADAPTIVE = 0, 1, 2, 3, 4, 5, 6, 7
 ALGOS = {"cqr2": CQR2, "cqr2gs": CQR2GS, "mcqr2gs": MCQR2GS, "cqr": CQR, "cqrgs": CQRGS, "scqr3": SCQR3,
-         "scqr": SCQR}
+         "scqr": SCQR, "mcqr2gs_adaptive": MCQR2GS_ADAPTIVE}
 TSQR_OK, TSQR_ERR_INVALID_ARG, TSQR_ERR_UNSUPPORTED, TSQR_ERR_CUDA = 0, 1, 2, 3
 TSQR_ERR_NCCL, TSQR_ERR_BREAKDOWN, TSQR_ERR_WORKSPACE = 4, 5, 6
 PLANES = ["local", "nccl", "fused"]
@@ -31,7 +31,7 @@ LIB_PATH = os.environ.get("TSQR_LIB", _build.LIB)  # override: timing experiment
 
 #: every function declared in include/tsqr.h
 EXPORTS = ["tsqr_workspace_bytes", "tsqr_create", "tsqr_factor", "tsqr_wait", "tsqr_last_counts",
-           "tsqr_factor_host", "tsqr_set_graph", "tsqr_data_plane", "tsqr_exec_path", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
+           "tsqr_factor_host", "tsqr_set_graph", "tsqr_data_plane", "tsqr_exec_path", "tsqr_set_adapt_tau", "tsqr_skipped_panels", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
            "tsqr_nccl_comm_init", "tsqr_nccl_comm_destroy", "tsqr_gram", "tsqr_proj", "tsqr_update",
            "tsqr_chol_inv", "tsqr_trmm"]
 
@@ -79,6 +79,8 @@ def load(build_if_missing: bool = False):
     L.tsqr_set_graph.argtypes = [_VP, _I32]
     L.tsqr_data_plane.argtypes = [_VP, ctypes.POINTER(_I32)]
     L.tsqr_exec_path.argtypes = [_VP, ctypes.POINTER(_I32)]
+    L.tsqr_set_adapt_tau.argtypes = [_VP, ctypes.c_double]
+    L.tsqr_skipped_panels.argtypes = [_VP, ctypes.POINTER(_I32)]
     L.tsqr_timing_reset.argtypes = [_VP]
     L.tsqr_timing.argtypes = [_VP, _I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                               ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
@@ -240,6 +242,16 @@ class Plan:
         v = _I32()
         _check(load().tsqr_exec_path(self.handle, ctypes.byref(v)), "tsqr_exec_path")
         return PATHS[v.value]
+
+    def set_adapt_tau(self, tau: float):
+        """mcqr2gs_adaptive: skip threshold of the repetition rule (0 never skips)."""
+        _check(load().tsqr_set_adapt_tau(self.handle, float(tau)), "tsqr_set_adapt_tau")
+
+    def skipped_panels(self) -> int:
+        """Panels whose CholeskyQR repetition the last factorisation skipped (after wait)."""
+        v = _I32()
+        _check(load().tsqr_skipped_panels(self.handle, ctypes.byref(v)), "tsqr_skipped_panels")
+        return v.value
 
     def set_timing(self, on: bool = True):
         _check(load().tsqr_set_timing(self.handle, 1 if on else 0), "tsqr_set_timing")

@@ -362,4 +362,61 @@ __global__ void k_zero2d(double* __restrict__ D, int64_t ldd, int rows, int cols
   }
 }
 
+// ---- runtime-adaptive repetition (TSQR_MCQR2GS_ADAPTIVE, DESIGN R-23) ----
+// status[0] codes: 0 running, 5 breakdown, 7 = "this panel's repetition is skipped": every
+// kernel checks failed(status) and returns at once, the fused cross-GPU sum keeps its barrier.
+constexpr int STATUS_SKIP = 7;
+
+// After the first CholeskyQR of a panel: E = max(u nu(U1)^2 nu(Z)^2, u nu(R_{1:j,j}) nu(Z)),
+// nu(M) = ||M||_F / sqrt(b) (Z = U1^{-1}, R_{1:j-1,j} = Rcol rows 0..c0-1).  E <= tau: mark the
+// skip (status[0] = 7, status[9] += 1) and prepare the R-8 bookkeeping to be exact no-ops:
+// U2 = I (R_jj = U2 U1 = U1 bitwise) and C = 0 (R_{1:j-1,j} += C U1 adds zeros).  One CTA,
+// fixed-order reduction: the decision is bitwise identical on every rank.
+__global__ void __launch_bounds__(256) k_adapt_decide(const double* __restrict__ U1, int ldu,
+                                                      const double* __restrict__ Z, int ldz,
+                                                      const double* __restrict__ Rcol, int ldr, int c0, int b,
+                                                      double tau, double* __restrict__ U2, int ldu2,
+                                                      double* __restrict__ C, int ldc, int* status) {
+  if (failed(status)) return;
+  __shared__ double red[3][256];
+  __shared__ int skip;
+  double su = 0.0, sz = 0.0, sy = 0.0;
+  for (int e = threadIdx.x; e < b * b; e += 256) {
+    const int i = e % b, j = e / b;
+    if (i <= j) {
+      const double u = U1[i + (int64_t)j * ldu], z = Z[i + (int64_t)j * ldz];
+      su = fma(u, u, su);
+      sz = fma(z, z, sz);
+    }
+  }
+  for (int e = threadIdx.x; e < c0 * b; e += 256) {
+    const double y = Rcol[(e % c0) + (int64_t)(e / c0) * ldr];
+    sy = fma(y, y, sy);
+  }
+  red[0][threadIdx.x] = su; red[1][threadIdx.x] = sz; red[2][threadIdx.x] = sy;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h)
+      for (int v = 0; v < 3; ++v) red[v][threadIdx.x] += red[v][threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double u = 1.1102230246251565e-16, bb = (double)b;
+    const double nu_u2 = red[0][0] / bb, nu_z2 = red[1][0] / bb, nu_r2 = (red[2][0] + red[0][0]) / bb;
+    const double own = u * nu_u2 * nu_z2, across = u * sqrt(nu_r2) * sqrt(nu_z2);
+    skip = (own > across ? own : across) <= tau;
+    if (skip) { status[9] += 1; status[0] = STATUS_SKIP; }
+  }
+  __syncthreads();
+  if (skip) {
+    for (int e = threadIdx.x; e < b * b; e += 256) U2[(e % b) + (int64_t)(e / b) * ldu2] = (e % b == e / b) ? 1.0 : 0.0;
+    for (int e = threadIdx.x; e < c0 * b; e += 256) C[(e % c0) + (int64_t)(e / c0) * ldc] = 0.0;
+  }
+}
+
+// end of a skippable section: a skip mark becomes "running" again (a breakdown stays)
+__global__ void k_adapt_resume(int* status) {
+  if (threadIdx.x == 0 && status[0] == STATUS_SKIP) status[0] = 0;
+}
+
 }  // namespace tsqr

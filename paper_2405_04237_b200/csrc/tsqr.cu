@@ -443,6 +443,23 @@ struct Launcher {
     return TSQR_OK;
   }
 
+  tsqr_status adapt_decide(const double* U1, const double* Z, const double* Rcol, int ldr, int c0, int b, double tau,
+                           double* U2, double* C) {
+    const size_t t0 = tbegin();
+    k_adapt_decide<<<1, 256, 0, st>>>(U1, b, Z, b, Rcol, ldr, c0, b, tau, U2, b, C, c0 > 0 ? c0 : 1,
+                                      const_cast<int*>(status));
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    tend(t0, TSQR_KCLASS_SMALL, 0.0, 0.0);
+    return TSQR_OK;
+  }
+  tsqr_status adapt_resume() {
+    k_adapt_resume<<<1, 32, 0, st>>>(const_cast<int*>(status));
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    return TSQR_OK;
+  }
+
   tsqr_status gemm_acc_tri(const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int p, int q) {
     const size_t t0 = tbegin();
     k_gemm_acc_tri<<<grid_1d((int64_t)p * q), 256, 0, st>>>(A, lda, B, ldb, Cm, ldc, p, q, status);
@@ -508,6 +525,7 @@ struct tsqr_plan_s {
   // tsqr_factor_host: per-panel "Q_j is final" events (recorded inside the graph as external
   // event nodes while capturing) so the device->host copy of Q_j overlaps the later panels
   bool panel_events = false, gpanel = false;
+  double adapt_tau = 8.8817841970012523e-16;  // 2^-50: TSQR_MCQR2GS_ADAPTIVE skip threshold (R-23)
   // single-launch cluster path for small problems (cluster_small.cuh)
   bool cluster = false;
   int cl_cs = 0;          // CTAs per cluster (16 or 8)
@@ -556,7 +574,7 @@ size_t max_part_doubles(int64_t m, int n, int b, tsqr_algo algo) {
   const int k = n / b;
   if (algo == TSQR_CQR2GS || algo == TSQR_CQRGS) {
     for (int j = 0; j + 1 < k; ++j) mx = std::max(mx, atb_part_doubles(m, b, n - (j + 1) * b, false));
-  } else if (algo == TSQR_MCQR2GS) {
+  } else if (algo == TSQR_MCQR2GS || algo == TSQR_MCQR2GS_ADAPTIVE) {
     for (int j = 1; j < k; ++j) {
       mx = std::max(mx, atb_part_doubles(m, b, n - j * b, false));
       mx = std::max(mx, atb_part_doubles(m, j * b, b, false));
@@ -587,7 +605,7 @@ tsqr_status check_shape(int64_t m_local, int n, int b, tsqr_algo algo) {
   if (m_local < 0 || n < 1 || n > 4096) { set_err("bad m_local/n"); return TSQR_ERR_INVALID_ARG; }
   // TMA tensor coordinates are 32-bit row indices
   if (m_local >= (int64_t(1) << 31)) { set_err("m_local >= 2^31 rows per rank unsupported"); return TSQR_ERR_UNSUPPORTED; }
-  if (algo < TSQR_CQR2 || algo > TSQR_SCQR) { set_err("bad algo"); return TSQR_ERR_INVALID_ARG; }
+  if (algo < TSQR_CQR2 || algo > TSQR_MCQR2GS_ADAPTIVE) { set_err("bad algo"); return TSQR_ERR_INVALID_ARG; }
   if (!valid_b(b)) { set_err("panel_b=%d not in {16,32,64,128,256}", b); return TSQR_ERR_UNSUPPORTED; }
   if (n % b != 0) { set_err("ragged panels (n %% b != 0) unsupported"); return TSQR_ERR_UNSUPPORTED; }
   if ((algo == TSQR_CQR2 || algo == TSQR_CQR || algo == TSQR_SCQR3 || algo == TSQR_SCQR) && b != n) {
@@ -656,11 +674,19 @@ tsqr_status update(tsqr_plan_s* P, double* X, int64_t ldx, const double* Lm, int
 }
 
 // CQR2 of the first b columns (Alg. 3; Alg. 8 l.1): U1, U2 -> R_11 = U2 U1
+// TSQR_MCQR2GS_ADAPTIVE: after the first CholeskyQR of a panel, decide on the device whether the
+// repetition is skipped (k_adapt_decide; R-23).  The skipped kernels still launch and return at
+// once (status[0] == 7) -- the graph and the allreduce sequence are the same on every call and
+// every rank.
+bool adaptive(const tsqr_plan_s* P) { return P->algo == TSQR_MCQR2GS_ADAPTIVE; }
+
 tsqr_status cqr2_block(tsqr_plan_s* P, double* A, int64_t lda, int w, double* R, int ldr) {
   TRY(gram(P, A, lda, w));
   TRY(chol_trmm(P, A, lda, w, P->U1, w, 1, 1, 1));
+  if (adaptive(P)) TRY(P->L.adapt_decide(P->U1, P->Z, R, ldr, 0, w, P->adapt_tau, P->U2, P->Y));
   TRY(gram(P, A, lda, w));
   TRY(chol_trmm(P, A, lda, w, P->U2, w, 1, 1, 2));
+  if (adaptive(P)) TRY(P->L.adapt_resume());
   return P->L.trimul(P->U2, w, P->U1, w, R, ldr, w);
 }
 
@@ -699,13 +725,15 @@ tsqr_status run_mcqr2gs(tsqr_plan_s* P, double* A, int64_t lda, double* R, int l
     // l.6: first CQR, panel -> V1, keep U1
     TRY(gram(P, Aj, lda, b));
     TRY(chol_trmm(P, Aj, lda, b, P->U1, b, 1, j + 1, 1));
-    // l.7: C = Q_{1:j-1}^T V1 ((j-1)b x b); V1 -= Q_{1:j-1} C
     const int jb = j * b;
+    if (adaptive(P)) TRY(P->L.adapt_decide(P->U1, P->Z, R + (int64_t)jb * ldr, ldr, jb, b, P->adapt_tau, P->U2, P->Y));
+    // l.7: C = Q_{1:j-1}^T V1 ((j-1)b x b); V1 -= Q_{1:j-1} C
     TRY(proj(P, A, lda, jb, Aj, lda, b, P->Y));
     TRY(update(P, Aj, lda, A, lda, P->Y, jb, jb, b));
     // l.8: second CQR -> Q_j, U2
     TRY(gram(P, Aj, lda, b));
     TRY(chol_trmm(P, Aj, lda, b, P->U2, b, 1, j + 1, 2));
+    if (adaptive(P)) TRY(P->L.adapt_resume());
     TRY(panel_done(P, j));
     // R_jj = U2 U1; R_{1:j-1,j} += C U1  (R-8)
     TRY(P->L.trimul(P->U2, b, P->U1, b, R + (int64_t)jb + (int64_t)jb * ldr, ldr, b));
@@ -810,7 +838,9 @@ cudaError_t cluster_config(size_t smem, int cs, int* active) {
 // blocks) plus the reduction buffers fit in the shared memory of CS CTAs.
 void setup_cluster_path(tsqr_plan_s* p) {
   const char* env = std::getenv("TSQR_CLUSTER_PATH");
-  if ((env && std::atoi(env) == 0) || p->comm || p->m < 1 || !(p->b == 16 || p->b == 32 || p->b == 64)) return;
+  if ((env && std::atoi(env) == 0) || p->comm || p->m < 1 || !(p->b == 16 || p->b == 32 || p->b == 64) ||
+      p->algo == TSQR_MCQR2GS_ADAPTIVE)
+    return;
   int dev = 0, optin = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
@@ -996,6 +1026,7 @@ static tsqr_status enqueue_factor(tsqr_plan_t P, double* A, int64_t lda, double*
       if (s == TSQR_OK) s = P->L.trimul(P->R2, n, P->R1, n, R, ldr, n);
       break;
     case TSQR_MCQR2GS:
+    case TSQR_MCQR2GS_ADAPTIVE:
       s = run_mcqr2gs(P, A, lda, R, ldr);
       break;
     case TSQR_SCQR3:
@@ -1134,7 +1165,8 @@ tsqr_status tsqr_factor_host(tsqr_plan_t P, double* A_host, int64_t lda_host, do
   // the panel-wise methods finalise Q one panel at a time: copy Q_j back on a second stream as
   // soon as it is final, overlapping the remaining panels (H2D has to complete first: the first
   // projection reads every column)
-  const bool by_panel = P->m > 0 && P->k > 1 && (P->algo == TSQR_MCQR2GS || P->algo == TSQR_CQR2GS);
+  const bool by_panel = P->m > 0 && P->k > 1 &&
+                        (P->algo == TSQR_MCQR2GS || P->algo == TSQR_MCQR2GS_ADAPTIVE || P->algo == TSQR_CQR2GS);
   if (!P->d2h) {
     CUDA_TRY(cudaStreamCreateWithFlags(&P->d2h, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&P->ev_d2h, cudaEventDisableTiming));
@@ -1204,6 +1236,26 @@ tsqr_status tsqr_timing(tsqr_plan_t P, int32_t kclass, double* ms, int64_t* laun
 tsqr_status tsqr_data_plane(tsqr_plan_t P, int32_t* plane) {
   if (!P || !plane) return TSQR_ERR_INVALID_ARG;
   *plane = P->L.ar_on ? TSQR_PLANE_FUSED : (P->comm ? TSQR_PLANE_NCCL : TSQR_PLANE_LOCAL);
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_set_adapt_tau(tsqr_plan_t P, double tau) {
+  if (!P || !(tau >= 0.0)) return TSQR_ERR_INVALID_ARG;
+  if (tau != P->adapt_tau && P->exec) {  // the threshold is a kernel argument of the captured graph
+    CUDA_TRY(cudaStreamSynchronize(P->gstream));
+    cudaGraphExecDestroy(P->exec);
+    P->exec = nullptr;
+  }
+  P->adapt_tau = tau;
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_skipped_panels(tsqr_plan_t P, int32_t* panels) {
+  if (!P || !panels) return TSQR_ERR_INVALID_ARG;
+  int h[16];
+  CUDA_TRY(cudaMemcpyAsync(h, P->status, sizeof(h), cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  *panels = P->algo == TSQR_MCQR2GS_ADAPTIVE ? h[9] : 0;
   return TSQR_OK;
 }
 

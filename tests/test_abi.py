@@ -62,7 +62,7 @@ def test_workspace_and_validation_without_gpu(lib):
     assert L.tsqr_workspace_bytes(4096, 64, 16, 1, t.CQR2) == 0         # CQR2 needs b == n
     assert L.tsqr_workspace_bytes(4096, 64, 16, 1, t.SCQR3) == 0        # sCQR3 needs b == n
     assert L.tsqr_workspace_bytes(4096, 64, 64, 1, t.SCQR3) > 0
-    assert L.tsqr_workspace_bytes(4096, 64, 64, 1, 7) == 0              # no such algorithm
+    assert L.tsqr_workspace_bytes(4096, 64, 64, 1, 8) == 0              # no such algorithm
     h = ctypes.c_void_p()
     rc = L.tsqr_create(ctypes.byref(h), 4096, 64, 16, None, t.MCQR2GS, None, None, 0)
     assert rc == t.TSQR_ERR_WORKSPACE and h.value is None

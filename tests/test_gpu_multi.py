@@ -111,7 +111,8 @@ PLANES = ["fused", "nccl"]
 @pytest.mark.parametrize("plane", PLANES)
 @pytest.mark.parametrize("algo,n,b,kappa", [("mcqr2gs", 256, 64, 1e8), ("mcqr2gs", 512, 64, 1e15),
                                              ("cqr2gs", 128, 32, 1e6), ("cqr2", 64, 64, 1e4),
-                                             ("scqr3", 128, 128, 1e12), ("mcqr2gs", 512, 128, 1e4)])
+                                             ("scqr3", 128, 128, 1e12), ("mcqr2gs", 512, 128, 1e4),
+                                             ("mcqr2gs_adaptive", 256, 32, 1e2)])
 def test_multi_rank_factorisation(algo, n, b, kappa, plane):
     _run_ranks(algo, n, b, kappa, plane=plane)
 

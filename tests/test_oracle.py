@@ -486,3 +486,87 @@ def test_scqr_shift_value_closed_form(orc):
     s = math.sqrt(m) * U_RND * n
     d = np.diag(R) ** 2 - 1.0
     assert np.max(np.abs(d / s - 1.0)) <= 0.01, (d.min() / s, d.max() / s)
+
+
+# ---------------------------------------------------------------- NEXT-f4: adaptive repetition
+# oracle.c mcqr2gs_adaptive (DESIGN R-23).  Pins: the two limits of the threshold are
+# existing algorithms bitwise; the estimate has closed forms; the default threshold keeps the
+# gates over a kappa sweep (frozen desk-scale observation) while skipping where kappa is small.
+
+@pytest.fixture
+def tau_guard(orc):
+    t = orc.get_adapt_tau()
+    yield
+    orc.set_adapt_tau(t)
+
+
+@pytest.mark.parametrize("m,n,b,kappa", [(4096, 128, 32, 1e3), (3001, 96, 32, 1e10), (2048, 64, 64, 1e2),
+                                         (5000, 100, 32, 1e6)])
+def test_adaptive_tau_zero_is_mcqr2gs_bitwise(orc, tau_guard, m, n, b, kappa):
+    A, _, _ = synth.generate_np(m, n, kappa, seed=2, chunk=m)
+    orc.set_adapt_tau(0.0)
+    Qa, Ra, ia = orc.factor(A, b, "mcqr2gs_adaptive")
+    Qm, Rm, im = orc.factor(A, b, "mcqr2gs")
+    assert orc.adapt_skipped() == 0
+    assert np.array_equal(Qa, Qm) and np.array_equal(Ra, Rm)
+
+
+@pytest.mark.parametrize("m,n,b,kappa", [(4096, 128, 32, 1e3), (3001, 96, 32, 1e10), (5000, 100, 32, 1e6)])
+def test_adaptive_tau_inf_is_cqrgs_bitwise(orc, tau_guard, m, n, b, kappa):
+    A, _, _ = synth.generate_np(m, n, kappa, seed=2, chunk=m)
+    orc.set_adapt_tau(math.inf)
+    Qa, Ra, _ = orc.factor(A, b, "mcqr2gs_adaptive")
+    Qc, Rc, _ = orc.factor(A, b, "cqrgs")
+    assert orc.adapt_skipped() == -(-n // b)
+    assert np.array_equal(Qa, Qc) and np.array_equal(Ra, Rc)
+
+
+def test_adaptive_estimate_closed_forms(orc):
+    """E = max(u nu(U)^2 nu(Z)^2, u nu([Rcol; U]) nu(Z)), nu(M) = ||M||_F / sqrt(b):
+    U = I, no column above: E = u exactly; U = diag(s): own = u (sum s^2/b)(sum s^-2/b);
+    a column block above adds to nu([Rcol; U]) only."""
+    import ctypes
+    L = orc.lib()
+    L.orc_adapt_estimate.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
+                                     ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_int64]
+    L.orc_adapt_estimate.restype = ctypes.c_double
+    P = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))  # noqa: E731
+    u = 2.0 ** -53
+    b = 8
+    I = np.asfortranarray(np.eye(b))
+    dummy = np.zeros((1, b), order="F")
+    assert L.orc_adapt_estimate(P(I), b, P(dummy), 1, 0) == u
+    s = 2.0 ** np.arange(b)  # powers of two: every sum below is exact
+    D = np.asfortranarray(np.diag(s))
+    own = u * (np.sum(s ** 2) / b) * (np.sum(s ** -2.0) / b)
+    assert L.orc_adapt_estimate(P(D), b, P(dummy), 1, 0) == pytest.approx(own, rel=1e-15)
+    Rc = np.asfortranarray(np.full((3, b), 4.0))  # ||Rcol||_F^2 = 3 b 16
+    across = u * math.sqrt((3 * b * 16 + b) / b) * 1.0
+    assert L.orc_adapt_estimate(P(I), b, P(Rc), 3, 3) == pytest.approx(across, rel=1e-15)
+    assert orc.kappa_f(D) == pytest.approx(math.sqrt(np.sum(s ** 2) * np.sum(s ** -2.0)), rel=1e-15)
+    assert orc.diag_ratio(D) == s[-1] / s[0]
+
+
+def test_adaptive_default_threshold_keeps_gates(orc, tau_guard):
+    """Frozen desk-scale observation (R-23): with the default tau = 2^-50 every case of the
+    kappa sweep meets the BJ gates; orthonormal-column inputs skip every repetition, kappa = 1e2
+    at least half of them (6 of 8 measured); at
+    kappa >= 1e12 nothing is skipped and the result is mCQR2GS bitwise."""
+    assert orc.get_adapt_tau() == 2.0 ** -50
+    m, n, b = 1 << 14, 256, 32
+    k = n // b
+    for kappa in (1.0, 1e2, 1e4, 1e8, 1e12, 1e15):
+        A, _, _ = synth.generate_np(m, n, kappa, seed=1)
+        Q, R, info = orc.factor(A, b, "mcqr2gs_adaptive")
+        sk = orc.adapt_skipped()
+        assert info["status"] == 0
+        assert orc.orthogonality(Q) <= 1e-13 and orc.residual(A, Q, R) <= 1e-14, kappa
+        assert np.array_equal(np.tril(R, -1), 0 * R) and np.all(np.diag(R) > 0)
+        if kappa == 1.0:
+            assert sk == k, sk
+        if kappa == 1e2:
+            assert sk >= k // 2, sk
+        if kappa >= 1e12:
+            assert sk == 0
+            Qm, Rm, _ = orc.factor(A, b, "mcqr2gs")
+            assert np.array_equal(Q, Qm) and np.array_equal(R, Rm)
