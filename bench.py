@@ -49,6 +49,18 @@ CONFIGS = {
     "scqr3-cfg2": (1 << 22, 256, 256, 1e12, "scqr3", "NEXT-f2: sCQR3 on the cfg2 shape (2^22 x 256, kappa=1e12: "
                    "at this m the conservative shift breaks down in the CQR2 stage from kappa ~1e14, R-22)"),
 }
+# NEXT-f3: the paper's strong-scaling workload (m = 120k, n = 1.2k / 6k / 12k, kappa = 1e4, 3 panels),
+# panel widths as multiples of 64 (R-24).  The FIRST field is the GLOBAL row count, split evenly over
+# the ranks (scaling "strong"); the generator's row chunk is fixed (15000) so the matrix does not
+# depend on the rank count.
+STRONG = {
+    "ss1k": (120000, 1152, 384, 1e4, "mcqr2gs", "NEXT-f3 strong scaling: m=120000 n=1152 (3 panels of 384) kappa=1e4"),
+    "ss6k": (120000, 6144, 2048, 1e4, "mcqr2gs", "NEXT-f3 strong scaling: m=120000 n=6144 (3 panels of 2048) kappa=1e4"),
+    "ss12k": (120000, 12288, 4096, 1e4, "mcqr2gs",
+              "NEXT-f3 strong scaling: m=120000 n=12288 (3 panels of 4096) kappa=1e4"),
+}
+CONFIGS.update(STRONG)
+STRONG_CHUNK = 15000
 
 
 def env_int(name, default):
@@ -181,6 +193,9 @@ def cpu_baseline(args, cfg):
     import oracle
     import synth
     m_local, n, b, kappa, algo, desc = cfg
+    if n > 2048:  # the oracle's O(m n^2) at n > 2048 does not fit a bounded CPU sample
+        return {"value": None, "unit": "TFLOP/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+                "sample": f"skipped: n = {n} too wide for a bounded oracle sample"}
     m_s = min(args.cpu_rows, m_local)
     A, _, _ = synth.generate_np(m_s, n, kappa, seed=0, chunk=min(m_s, 65536))
     cores = len(os.sched_getaffinity(0))
@@ -251,12 +266,19 @@ def main():
         comm = tsqr.NcclComm(rank, world, local)
 
     m_local, n, b, kappa, algo, desc = cfg
-    m_global = m_local * world
+    strong = args.config in STRONG
+    if strong:  # fixed global problem split over the ranks
+        m_global = m_local
+        m_local = m_global // world
+        chunk = STRONG_CHUNK
+    else:
+        m_global = m_local * world
+        chunk = 65536
     peaks = load_peaks()
 
     # ---- inputs: rows [rank*m_local, (rank+1)*m_local) of the global seeded test matrix
     A = tsqr.colmajor_empty(m_local, n, device=dev)
-    synth.generate_torch(A, m_global, rank * m_local, n, kappa, seed=args.seed)
+    synth.generate_torch(A, m_global, rank * m_local, n, kappa, seed=args.seed, chunk=chunk)
     A0 = tsqr.colmajor_empty(m_local, n, device=dev)
     A0.copy_(A)
     R = tsqr.colmajor_empty(n, n, device=dev)
@@ -380,7 +402,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded A = U diag(sigma) V^T with log-spaced sigma, P:108)",
             "config": {"workload": desc, "config": args.config, "m_local": m_local, "m_global": m_global, "n": n,
                        "b": b, "kappa": kappa, "algo": algo, "parallelism": f"row-sharded dp{world}",

@@ -100,10 +100,11 @@ size_t tsqr_workspace_bytes(int64_t m_local, int32_t n, int32_t panel_b, int32_t
  * same n, panel_b and algo; m_local may differ per rank).  When nccl_comm is NULL
  * the plan is single-GPU (P = 1).
  *   m_local        rows owned by this rank, >= 0 (sum over ranks >= n)
- *   n              columns, 1 <= n <= 4096
- *   panel_b        panel width b: required n % b == 0 and
- *                  b in {16, 32, 64, 128, 256}; for CQR / CQR2, b must equal n and
- *                  n <= 256 (single panel).  Ragged panels: TSQR_ERR_UNSUPPORTED.
+ *   n              columns, 1 <= n <= 16384
+ *   panel_b        panel width b: required n % b == 0 and b = 16, 32 or a
+ *                  multiple of 64 up to 4096 (the paper's 400-4000-wide strong-scaling panels,
+ *                  P:504, as multiples of 64: DESIGN R-24); for CQR / CQR2 / sCQR(3), b must
+ *                  equal n (single panel).  Ragged panels: TSQR_ERR_UNSUPPORTED.
  *   nccl_comm      ncclComm_t (see tsqr_nccl_comm_init) or NULL
  *   algo           method, see tsqr_algo
  *   cuda_stream    cudaStream_t every launch and NCCL call is enqueued on (NULL =
@@ -266,7 +267,8 @@ tsqr_status tsqr_update(double* X, int64_t ldx, const double* L, int64_t ldl, co
  * (Alg. 1 l.2; R-4, R-5).  W b x b (only the upper triangle is read);
  * U and Z receive exact zeros below the diagonal.  On breakdown *status_dev
  * (device int32[8]) is set to {1, pivot, ...} with the pivot value in
- * status_dev[2..3] as a double; otherwise it is left untouched.  b <= 256. */
+ * status_dev[2..3] as a double; otherwise it is left untouched.  b: 16, 32 or a multiple of 64
+ * up to 4096 (b > 256: multi-CTA blocked kernels, one launch per block step). */
 tsqr_status tsqr_chol_inv(const double* W, int32_t ldw, int32_t b, double* U, int32_t ldu, double* Z,
                           int32_t ldz, int32_t* status_dev, void* cuda_stream);
 

@@ -299,6 +299,103 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_inv_blocked(const double* _
 }
 
 // -----------------------------------------------------------------------------------------
+// Multi-CTA blocked Cholesky + inverse for wide panels (b = 64 nb > 256, the
+// strong-scaling panels of 400-4000 columns): the same right-looking blocked algorithm
+// as k_chol_inv_blocked (R-5), one launch per step so the independent blocks of a step run
+// on separate CTAs:
+//   prep:           work <- upper(W); U, Z <- 0
+//   for J:  diag:   U_JJ = chol(W_JJ), Z_JJ = U_JJ^{-1}                       (1 CTA)
+//           row:    U_JK = Z_JJ^T W_JK, K > J                                (nb-J-1 CTAs)
+//           trail:  W_KL -= U_JK^T U_JL, J < K <= L                          ((nb-J-1)(nb-J)/2 CTAs)
+//   for d = 1..nb-1: Z_IJ = -Z_II sum_{K=I+1..J} U_IK Z_KJ, J - I = d        (nb-d CTAs; R-4)
+// Blocks are staged through shared memory with the 512-thread block primitives above; the
+// breakdown (status) is reported with the global pivot index, later kernels return at once.
+// -----------------------------------------------------------------------------------------
+__global__ void k_chol_prep(const double* __restrict__ W, int ldw, int b, double* __restrict__ work,
+                            double* __restrict__ U, int ldu, double* __restrict__ Z, int ldz, const int* status) {
+  if (failed(status)) return;
+  const int64_t bb = (int64_t)b * b;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % b), j = (int)(e / b);
+    work[e] = (i <= j) ? W[i + (int64_t)j * ldw] : 0.0;
+    U[i + (int64_t)j * ldu] = 0.0;
+    Z[i + (int64_t)j * ldz] = 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(CHOL_NT, 1) k_chol_diag(const double* __restrict__ work, int b, int J,
+                                                          double* __restrict__ U, int ldu, double* __restrict__ Z,
+                                                          int ldz, int* status, int pass, int panel, int stage) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double s_urow[CHB];
+  if (failed(status)) return;
+  const int tid = threadIdx.x;
+  double* D = smem;
+  double* Di = smem + CHB * CHLD;
+  blk_load(D, work + (int64_t)J * CHB * b + J * CHB, b, tid);
+  if (!blk_chol_inv(D, Di, s_urow, status, pass, panel, stage, J * CHB, tid)) return;
+  blk_store(U + (int64_t)J * CHB * ldu + J * CHB, ldu, D, tid);
+  blk_store(Z + (int64_t)J * CHB * ldz + J * CHB, ldz, Di, tid);
+}
+
+__global__ void __launch_bounds__(CHOL_NT, 1) k_chol_row(const double* __restrict__ work, int b, int J,
+                                                         double* __restrict__ U, int ldu, const double* __restrict__ Z,
+                                                         int ldz, const int* status) {
+  extern __shared__ __align__(16) double smem[];
+  if (failed(status)) return;
+  const int tid = threadIdx.x, K = J + 1 + blockIdx.x;
+  double* Di = smem;
+  double* T = smem + CHB * CHLD;
+  double* PK = smem + 2 * CHB * CHLD;
+  blk_load(Di, Z + (int64_t)J * CHB * ldz + J * CHB, ldz, tid);
+  blk_load(T, work + (int64_t)K * CHB * b + J * CHB, b, tid);
+  blk_mm<true, false>(Di, T, PK, tid);
+  blk_store(U + (int64_t)K * CHB * ldu + J * CHB, ldu, PK, tid);
+}
+
+__global__ void __launch_bounds__(CHOL_NT, 1) k_chol_trail(double* __restrict__ work, int b, int J,
+                                                           const double* __restrict__ U, int ldu, const int* status) {
+  extern __shared__ __align__(16) double smem[];
+  if (failed(status)) return;
+  const int tid = threadIdx.x, r = (b / CHB) - J - 1;
+  // blockIdx.x -> (K, L), J < K <= L < nb, enumerated column by column of the trailing triangle
+  int t = blockIdx.x, L2 = 0;
+  while (t >= L2 + 1) { t -= L2 + 1; ++L2; }
+  const int K = J + 1 + t, L = J + 1 + L2;
+  (void)r;
+  double* A = smem;
+  double* B = smem + CHB * CHLD;
+  double* T = smem + 2 * CHB * CHLD;
+  double* wkl = work + (int64_t)L * CHB * b + K * CHB;
+  blk_load(A, U + (int64_t)K * CHB * ldu + J * CHB, ldu, tid);
+  blk_load(B, U + (int64_t)L * CHB * ldu + J * CHB, ldu, tid);
+  blk_load(T, wkl, b, tid);
+  blk_mm<true, true>(A, B, T, tid);
+  blk_store(wkl, b, T, tid);
+}
+
+__global__ void __launch_bounds__(CHOL_NT, 1) k_tri_inv_step(const double* __restrict__ U, int ldu,
+                                                             double* __restrict__ Z, int ldz, int d, const int* status) {
+  extern __shared__ __align__(16) double smem[];
+  if (failed(status)) return;
+  const int tid = threadIdx.x, I = blockIdx.x, J = I + d;
+  double* D = smem;
+  double* Di = smem + CHB * CHLD;
+  double* P = smem + 2 * CHB * CHLD;
+  double* T = smem + 3 * CHB * CHLD;
+  for (int e = tid; e < CHB * CHB; e += CHOL_NT) P[(e & 63) + (e >> 6) * CHLD] = 0.0;
+  __syncthreads();
+  for (int K = I + 1; K <= J; ++K) {
+    blk_load(D, U + (int64_t)K * CHB * ldu + I * CHB, ldu, tid);   // U_IK
+    blk_load(Di, Z + (int64_t)J * CHB * ldz + K * CHB, ldz, tid);  // Z_KJ
+    blk_mm<false, true>(D, Di, P, tid);                             // P -= U_IK Z_KJ
+  }
+  blk_load(D, Z + (int64_t)I * CHB * ldz + I * CHB, ldz, tid);     // Z_II
+  blk_mm<false, false>(D, P, T, tid);                              // Z_IJ = Z_II (-S)
+  blk_store(Z + (int64_t)J * CHB * ldz + I * CHB, ldz, T, tid);
+}
+
+// -----------------------------------------------------------------------------------------
 // R assembly (Alg. 3 l.3 P:185; Alg. 6 l.5/l.8 P:295/P:298; R-8).  Negligible work.
 // -----------------------------------------------------------------------------------------
 // C (n x n) = A * B for upper-triangular A, B: C[i,j] = sum_{t=i..j} A[i,t] B[t,j]; zeros below.

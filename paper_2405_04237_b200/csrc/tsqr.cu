@@ -77,7 +77,9 @@ constexpr size_t kAlign = 256;
 
 size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
-bool valid_b(int b) { return b == 16 || b == 32 || b == 64 || b == 128 || b == 256; }
+// panel widths: 16, 32, or any multiple of 64 up to 4096 (b > 256: the wide panels of the paper's
+// strong-scaling workload, with the multi-CTA blocked Cholesky; DESIGN R-24)
+bool valid_b(int b) { return b == 16 || b == 32 || (b % 64 == 0 && b >= 64 && b <= 4096); }
 
 // ---- split-row policy of k_atb (a function of the problem only -> deterministic) ----
 struct AtbShape {
@@ -409,6 +411,29 @@ struct Launcher {
   tsqr_status chol_inv(const double* W, int ldw, int b, double* U, int ldu, double* Z, int ldz, int* status_rw,
                        int pass, int panel, int stage, double* work) {
     const size_t t0 = tbegin();
+    if (b > 256 && b % 64 == 0 && work) {  // wide panels: multi-CTA blocked variant, one launch per step
+      const int nb = b / CHB;
+      CUDA_TRY(set_smem(k_chol_diag, CHOL_BLK_SMEM));
+      CUDA_TRY(set_smem(k_chol_row, CHOL_BLK_SMEM));
+      CUDA_TRY(set_smem(k_chol_trail, CHOL_BLK_SMEM));
+      CUDA_TRY(set_smem(k_tri_inv_step, CHOL_BLK_SMEM));
+      k_chol_prep<<<grid_1d((int64_t)b * b), 256, 0, st>>>(W, ldw, b, work, U, ldu, Z, ldz, status_rw);
+      launches += 1;
+      for (int J = 0; J < nb; ++J) {
+        k_chol_diag<<<1, CHOL_NT, CHOL_BLK_SMEM, st>>>(work, b, J, U, ldu, Z, ldz, status_rw, pass, panel, stage);
+        const int r = nb - J - 1;
+        if (r > 0) {
+          k_chol_row<<<r, CHOL_NT, CHOL_BLK_SMEM, st>>>(work, b, J, U, ldu, Z, ldz, status_rw);
+          k_chol_trail<<<r * (r + 1) / 2, CHOL_NT, CHOL_BLK_SMEM, st>>>(work, b, J, U, ldu, status_rw);
+        }
+        launches += r > 0 ? 3 : 1;
+      }
+      for (int d = 1; d < nb; ++d) k_tri_inv_step<<<nb - d, CHOL_NT, CHOL_BLK_SMEM, st>>>(U, ldu, Z, ldz, d, status_rw);
+      launches += nb - 1;
+      CUDA_TRY(cudaGetLastError());
+      tend(t0, TSQR_KCLASS_CHOL, 2.0 * b * b * b / 3.0, 16.0 * b * b);
+      return TSQR_OK;
+    }
     if (b >= 128 && b % 64 == 0 && work) {  // blocked variant (64x64 blocks, W staged in `work`)
       CUDA_TRY(set_smem(k_chol_inv_blocked, CHOL_BLK_SMEM));
       k_chol_inv_blocked<<<1, CHOL_NT, CHOL_BLK_SMEM, st>>>(W, ldw, b, U, ldu, Z, ldz, status_rw, pass, panel, stage,
@@ -602,11 +627,11 @@ size_t carve(Carve& c, tsqr_plan_s* p, int64_t m, int n, int b, tsqr_algo algo) 
 }
 
 tsqr_status check_shape(int64_t m_local, int n, int b, tsqr_algo algo) {
-  if (m_local < 0 || n < 1 || n > 4096) { set_err("bad m_local/n"); return TSQR_ERR_INVALID_ARG; }
+  if (m_local < 0 || n < 1 || n > 16384) { set_err("bad m_local/n"); return TSQR_ERR_INVALID_ARG; }
   // TMA tensor coordinates are 32-bit row indices
   if (m_local >= (int64_t(1) << 31)) { set_err("m_local >= 2^31 rows per rank unsupported"); return TSQR_ERR_UNSUPPORTED; }
   if (algo < TSQR_CQR2 || algo > TSQR_MCQR2GS_ADAPTIVE) { set_err("bad algo"); return TSQR_ERR_INVALID_ARG; }
-  if (!valid_b(b)) { set_err("panel_b=%d not in {16,32,64,128,256}", b); return TSQR_ERR_UNSUPPORTED; }
+  if (!valid_b(b)) { set_err("panel_b=%d not 16, 32 or a multiple of 64 up to 4096", b); return TSQR_ERR_UNSUPPORTED; }
   if (n % b != 0) { set_err("ragged panels (n %% b != 0) unsupported"); return TSQR_ERR_UNSUPPORTED; }
   if ((algo == TSQR_CQR2 || algo == TSQR_CQR || algo == TSQR_SCQR3 || algo == TSQR_SCQR) && b != n) {
     set_err("CQR/CQR2/sCQR/sCQR3 need b == n");
