@@ -408,6 +408,26 @@ struct Launcher {
     return TSQR_OK;
   }
 
+  // Z = U^{-1} on the 64-block range [lo, hi) by recursive halving (the diagonal blocks Z_II come
+  // from k_chol_diag): inv([A B; 0 C]) = [A^-1, -A^-1 B C^-1; 0, C^-1] (R-4), the two products of
+  // every split on the DMMA update kernel: T = 0; T -= Z_AA U_AC; T = -T; Z_AC -= T Z_CC.
+  // (A chain of block back-substitutions would serialise ~nb^2/2 block products; the halving
+  // needs log2(nb) dependent levels of large GEMMs.)  T uses `work` (b x b, ld b).
+  tsqr_status tri_inv_rec(const double* U, int ldu, double* Z, int ldz, int b, int lo, int hi, double* work) {
+    if (hi - lo < 2) return TSQR_OK;
+    const int mid = lo + (hi - lo) / 2;
+    TRY(tri_inv_rec(U, ldu, Z, ldz, b, lo, mid, work));
+    TRY(tri_inv_rec(U, ldu, Z, ldz, b, mid, hi, work));
+    const int a0 = lo * CHB, c0 = mid * CHB, sa = (mid - lo) * CHB, sc = (hi - mid) * CHB;
+    double* T = work;
+    k_zero2d<<<grid_1d((int64_t)sa * sc), 256, 0, st>>>(T, b, sa, sc);
+    CUDA_TRY(cudaGetLastError());
+    launches += 1;
+    TRY(update(T, b, Z + a0 + (int64_t)a0 * ldz, ldz, U + a0 + (int64_t)c0 * ldu, ldu, sa, sa, sc));
+    TRY(copy2d(T, b, T, b, sa, sc, -1.0));
+    return update(Z + a0 + (int64_t)c0 * ldz, ldz, T, b, Z + c0 + (int64_t)c0 * ldz, ldz, sa, sc, sc);
+  }
+
   tsqr_status chol_inv(const double* W, int ldw, int b, double* U, int ldu, double* Z, int ldz, int* status_rw,
                        int pass, int panel, int stage, double* work) {
     const size_t t0 = tbegin();
@@ -428,9 +448,13 @@ struct Launcher {
         }
         launches += r > 0 ? 3 : 1;
       }
-      for (int d = 1; d < nb; ++d) k_tri_inv_step<<<nb - d, CHOL_NT, CHOL_BLK_SMEM, st>>>(U, ldu, Z, ldz, d, status_rw);
-      launches += nb - 1;
       CUDA_TRY(cudaGetLastError());
+      Timer* tm = timer;
+      timer = nullptr;  // the inverse's update launches are part of this Cholesky's timed range
+      const tsqr_status si = tri_inv_rec(U, ldu, Z, ldz, b, 0, nb, work);
+      timer = tm;
+      TRY(si);
+
       tend(t0, TSQR_KCLASS_CHOL, 2.0 * b * b * b / 3.0, 16.0 * b * b);
       return TSQR_OK;
     }
@@ -459,7 +483,18 @@ struct Launcher {
     return TSQR_OK;
   }
 
-  tsqr_status trimul(const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int n) {
+  // Cm (n x n) = A B for upper-triangular A, B.  n >= 512 (wide panels, NEXT-f3): a dense DMMA
+  // product through the update kernel -- Cm = 0, A <- -A IN PLACE (every caller passes a factor
+  // that is dead afterwards: U2, R2), Cm -= (-A) B -- instead of one thread per entry (the
+  // triangular zeros stay exact zeros: their products are exact).
+  tsqr_status trimul(double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int n) {
+    if (n >= 512) {
+      k_zero2d<<<grid_1d((int64_t)n * n), 256, 0, st>>>(Cm, ldc, n, n);
+      CUDA_TRY(cudaGetLastError());
+      launches += 1;
+      TRY(copy2d(A, lda, A, lda, n, n, -1.0));
+      return update(Cm, ldc, A, lda, B, ldb, n, n, n);
+    }
     const size_t t0 = tbegin();
     k_trimul<<<grid_1d((int64_t)n * n), 256, 0, st>>>(A, lda, B, ldb, Cm, ldc, n, status);
     CUDA_TRY(cudaGetLastError());
@@ -485,7 +520,13 @@ struct Launcher {
     return TSQR_OK;
   }
 
-  tsqr_status gemm_acc_tri(const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int p, int q) {
+  // Cm (p x q) += A (p x q) B (q x q upper).  q >= 512: A <- -A IN PLACE (the dead C block),
+  // then the update kernel Cm -= (-A) B.
+  tsqr_status gemm_acc_tri(double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int p, int q) {
+    if (q >= 512) {
+      TRY(copy2d(A, lda, A, lda, p, q, -1.0));
+      return update(Cm, ldc, A, lda, B, ldb, p, q, q);
+    }
     const size_t t0 = tbegin();
     k_gemm_acc_tri<<<grid_1d((int64_t)p * q), 256, 0, st>>>(A, lda, B, ldb, Cm, ldc, p, q, status);
     CUDA_TRY(cudaGetLastError());
@@ -1389,7 +1430,8 @@ tsqr_status tsqr_update(double* X, int64_t ldx, const double* Lm, int64_t ldl, c
 
 tsqr_status tsqr_chol_inv(const double* W, int32_t ldw, int32_t b, double* U, int32_t ldu, double* Z, int32_t ldz,
                           int32_t* status_dev, void* cuda_stream) {
-  if (!W || !U || !Z || !status_dev || b < 1 || b > 256 || ldw < b || ldu < b || ldz < b) return TSQR_ERR_INVALID_ARG;
+  if (!W || !U || !Z || !status_dev || b < 1 || b > 4096 || ldw < b || ldu < b || ldz < b) return TSQR_ERR_INVALID_ARG;
+  if (b > 256 && b % 64 != 0) return TSQR_ERR_UNSUPPORTED;
   Launcher L;
   L.st = reinterpret_cast<cudaStream_t>(cuda_stream);
   double* work = nullptr;
