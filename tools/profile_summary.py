@@ -20,7 +20,9 @@ dst = os.path.join(ROOT, "profiles", tag)
 os.makedirs(dst, exist_ok=True)
 
 CLASS = {"k_update": "update", "k_update_pp": "update", "k_proj": "proj", "k_trmm": "trmm", "k_chol_inv": "chol",
-         "k_chol_inv_blocked": "chol", "k_reduce": "reduce"}
+         "k_chol_inv_blocked": "chol", "k_reduce": "reduce", "k_reduce_allreduce": "allreduce",
+         "k_cluster_factor": "cluster", "k_chol_prep": "chol", "k_chol_diag": "chol", "k_chol_row": "chol",
+         "k_chol_trail": "chol", "k_adapt_decide": "small", "k_adapt_resume": "small"}
 
 
 def unit_scale(u):
