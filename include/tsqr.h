@@ -187,6 +187,16 @@ tsqr_status tsqr_timing(tsqr_plan_t plan, int32_t kclass, double* ms, int64_t* l
  * enable = 0 switches to eager enqueueing. */
 tsqr_status tsqr_set_graph(tsqr_plan_t plan, int32_t enable);
 
+/* NEXT-f1 look-ahead ("overlap the update of panels with computing the CholeskyQR of the
+ * next panel (Algorithm 8 lines 4 and 6)"), TSQR_MCQR2GS on the streaming path with >= 3 panels:
+ * after the projection of step j the panel's own columns are updated first, its CholeskyQR chain
+ * (l.6-8, incl. the cross-GPU sums) then runs on a second stream while the main stream updates
+ * the remaining trailing columns; the two join before step j+1.  The same kernels on the same
+ * operands: Q and R are bitwise those of the serial schedule.  enable = 0 (default; also
+ * TSQR_LOOKAHEAD=1 at tsqr_create) / 1; silently off where it does not apply.  COLLECTIVE in
+ * effect: every rank must use the same setting (the allreduce order is unchanged). */
+tsqr_status tsqr_set_lookahead(tsqr_plan_t plan, int32_t enable);
+
 /* TSQR_MCQR2GS_ADAPTIVE: threshold tau of the skip rule (default 2^-50 ~ 8.9e-16; 0 never
  * skips).  Takes effect at the next tsqr_factor (it re-captures the CUDA graph). */
 tsqr_status tsqr_set_adapt_tau(tsqr_plan_t plan, double tau);

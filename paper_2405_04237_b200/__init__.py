@@ -31,7 +31,7 @@ LIB_PATH = os.environ.get("TSQR_LIB", _build.LIB)  # override: timing experiment
 
 #: every function declared in include/tsqr.h
 EXPORTS = ["tsqr_workspace_bytes", "tsqr_create", "tsqr_factor", "tsqr_wait", "tsqr_last_counts",
-           "tsqr_factor_host", "tsqr_set_graph", "tsqr_data_plane", "tsqr_exec_path", "tsqr_set_adapt_tau", "tsqr_skipped_panels", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
+           "tsqr_factor_host", "tsqr_set_graph", "tsqr_data_plane", "tsqr_exec_path", "tsqr_set_adapt_tau", "tsqr_skipped_panels", "tsqr_set_lookahead", "tsqr_set_timing", "tsqr_timing_reset", "tsqr_timing", "tsqr_destroy", "tsqr_status_string", "tsqr_last_error", "tsqr_nccl_unique_id",
            "tsqr_nccl_comm_init", "tsqr_nccl_comm_destroy", "tsqr_gram", "tsqr_proj", "tsqr_update",
            "tsqr_chol_inv", "tsqr_trmm"]
 
@@ -80,6 +80,7 @@ def load(build_if_missing: bool = False):
     L.tsqr_data_plane.argtypes = [_VP, ctypes.POINTER(_I32)]
     L.tsqr_exec_path.argtypes = [_VP, ctypes.POINTER(_I32)]
     L.tsqr_set_adapt_tau.argtypes = [_VP, ctypes.c_double]
+    L.tsqr_set_lookahead.argtypes = [_VP, _I32]
     L.tsqr_skipped_panels.argtypes = [_VP, ctypes.POINTER(_I32)]
     L.tsqr_timing_reset.argtypes = [_VP]
     L.tsqr_timing.argtypes = [_VP, _I32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
@@ -242,6 +243,10 @@ class Plan:
         v = _I32()
         _check(load().tsqr_exec_path(self.handle, ctypes.byref(v)), "tsqr_exec_path")
         return PATHS[v.value]
+
+    def set_lookahead(self, on: bool = True):
+        """NEXT-f1: run each panel's CholeskyQR chain on a second stream under the trailing update."""
+        _check(load().tsqr_set_lookahead(self.handle, 1 if on else 0), "tsqr_set_lookahead")
 
     def set_adapt_tau(self, tau: float):
         """mcqr2gs_adaptive: skip threshold of the repetition rule (0 never skips)."""

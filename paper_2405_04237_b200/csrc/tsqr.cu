@@ -563,6 +563,7 @@ struct tsqr_plan_s {
   double* part = nullptr;    // split-row partials
   double* W = nullptr;       // Gram block (b x b)
   double* Y = nullptr;       // projection block (b x n) / (n x b)
+  double* C = nullptr;       // re-orthogonalisation block C ((j-1)b x b) of mCQR2GS l.7
   double* U1 = nullptr;      // b x b
   double* U2 = nullptr;      // b x b
   double* Z = nullptr;       // b x b inverse
@@ -592,6 +593,11 @@ struct tsqr_plan_s {
   // event nodes while capturing) so the device->host copy of Q_j overlaps the later panels
   bool panel_events = false, gpanel = false;
   double adapt_tau = 8.8817841970012523e-16;  // 2^-50: TSQR_MCQR2GS_ADAPTIVE skip threshold (R-23)
+  // NEXT-f1 look-ahead (mCQR2GS): panel j's CholeskyQR chain (Alg. 8 l.6-8) on a second stream
+  // while the rest of the trailing update (l.4) runs on the main one
+  bool lookahead = false;
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev_fork, ev_join;
   // single-launch cluster path for small problems (cluster_small.cuh)
   bool cluster = false;
   int cl_cs = 0;          // CTAs per cluster (16 or 8)
@@ -618,6 +624,10 @@ struct tsqr_plan_s {
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);
     if (gstream) cudaStreamDestroy(gstream);
+    if (side) cudaStreamSynchronize(side);
+    for (cudaEvent_t e : ev_fork) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -654,6 +664,7 @@ size_t carve(Carve& c, tsqr_plan_s* p, int64_t m, int n, int b, tsqr_algo algo) 
   double* part = c.take<double>(max_part_doubles(m, n, b, algo));
   double* W = c.take<double>((size_t)b * b);
   double* Y = c.take<double>((size_t)b * n);
+  double* Cb = c.take<double>((size_t)b * n);  // mCQR2GS l.7 block C (look-ahead: Y stays live meanwhile)
   double* U1 = c.take<double>((size_t)b * b);
   double* U2 = c.take<double>((size_t)b * b);
   double* Z = c.take<double>((size_t)b * b);
@@ -661,7 +672,7 @@ size_t carve(Carve& c, tsqr_plan_s* p, int64_t m, int n, int b, tsqr_algo algo) 
   double* R2 = c.take<double>((size_t)n * n);
   double* cw = c.take<double>((size_t)b * b);
   if (p) {
-    p->status = status; p->part = part; p->W = W; p->Y = Y; p->U1 = U1; p->U2 = U2; p->Z = Z;
+    p->status = status; p->part = part; p->W = W; p->Y = Y; p->C = Cb; p->U1 = U1; p->U2 = U2; p->Z = Z;
     p->R1 = R1; p->R2 = R2; p->cwork = cw;
   }
   return align_up(c.off);
@@ -780,22 +791,37 @@ tsqr_status run_mcqr2gs(tsqr_plan_s* P, double* A, int64_t lda, double* R, int l
   const int n = P->n, b = P->b, k = P->k;
   TRY(cqr2_block(P, A, lda, b, R, ldr));                                      // l.1
   TRY(panel_done(P, 0));
+  cudaStream_t main_st = P->L.st;
   for (int j = 1; j < k; ++j) {
     double* Ap = A + (int64_t)(j - 1) * b * lda;  // Q_{j-1}
     double* Aj = A + (int64_t)j * b * lda;
     const int Nj = n - j * b;
     // l.3-5: Y = Q_{j-1}^T A_{:,j:k}; A_{:,j:k} -= Q_{j-1} Y; R_{j-1,j:k} = Y
     TRY(proj(P, Ap, lda, b, Aj, lda, Nj, P->Y));
-    TRY(update(P, Aj, lda, Ap, lda, P->Y, b, b, Nj));
     TRY(P->L.copy2d(P->Y, b, R + (int64_t)(j - 1) * b + (int64_t)j * b * ldr, ldr, b, Nj));
+    const bool fork = P->lookahead && Nj > b;
+    if (fork) {
+      // look-ahead: update panel j's own columns first, then run its CholeskyQR chain
+      // (l.6-8) on the side stream while the main stream updates columns j+1..k.  The same
+      // kernels on the same operands (every output column's arithmetic is independent of the
+      // launch's column range), so the result is bitwise that of the serial schedule.
+      TRY(update(P, Aj, lda, Ap, lda, P->Y, b, b, b));
+      CUDA_TRY(cudaEventRecord(P->ev_fork[j], main_st));
+      CUDA_TRY(cudaStreamWaitEvent(P->side, P->ev_fork[j], 0));
+      P->L.st = main_st;
+      TRY(update(P, Aj + (int64_t)b * lda, lda, Ap, lda, P->Y + (int64_t)b * b, b, b, Nj - b));
+      P->L.st = P->side;
+    } else {
+      TRY(update(P, Aj, lda, Ap, lda, P->Y, b, b, Nj));
+    }
     // l.6: first CQR, panel -> V1, keep U1
     TRY(gram(P, Aj, lda, b));
     TRY(chol_trmm(P, Aj, lda, b, P->U1, b, 1, j + 1, 1));
     const int jb = j * b;
-    if (adaptive(P)) TRY(P->L.adapt_decide(P->U1, P->Z, R + (int64_t)jb * ldr, ldr, jb, b, P->adapt_tau, P->U2, P->Y));
+    if (adaptive(P)) TRY(P->L.adapt_decide(P->U1, P->Z, R + (int64_t)jb * ldr, ldr, jb, b, P->adapt_tau, P->U2, P->C));
     // l.7: C = Q_{1:j-1}^T V1 ((j-1)b x b); V1 -= Q_{1:j-1} C
-    TRY(proj(P, A, lda, jb, Aj, lda, b, P->Y));
-    TRY(update(P, Aj, lda, A, lda, P->Y, jb, jb, b));
+    TRY(proj(P, A, lda, jb, Aj, lda, b, P->C));
+    TRY(update(P, Aj, lda, A, lda, P->C, jb, jb, b));
     // l.8: second CQR -> Q_j, U2
     TRY(gram(P, Aj, lda, b));
     TRY(chol_trmm(P, Aj, lda, b, P->U2, b, 1, j + 1, 2));
@@ -803,7 +829,12 @@ tsqr_status run_mcqr2gs(tsqr_plan_s* P, double* A, int64_t lda, double* R, int l
     TRY(panel_done(P, j));
     // R_jj = U2 U1; R_{1:j-1,j} += C U1  (R-8)
     TRY(P->L.trimul(P->U2, b, P->U1, b, R + (int64_t)jb + (int64_t)jb * ldr, ldr, b));
-    TRY(P->L.gemm_acc_tri(P->Y, jb, P->U1, b, R + (int64_t)jb * ldr, ldr, jb, b));
+    TRY(P->L.gemm_acc_tri(P->C, jb, P->U1, b, R + (int64_t)jb * ldr, ldr, jb, b));
+    if (fork) {  // join: step j+1 projects against Q_j (side) and the updated columns (main)
+      CUDA_TRY(cudaEventRecord(P->ev_join[j], P->side));
+      CUDA_TRY(cudaStreamWaitEvent(main_st, P->ev_join[j], 0));
+      P->L.st = main_st;
+    }
   }
   return TSQR_OK;
 }
@@ -1054,6 +1085,13 @@ tsqr_status tsqr_create(tsqr_plan_t* plan, int64_t m_local, int32_t n, int32_t p
     }
   }
   setup_cluster_path(p);
+  {
+    const char* la = std::getenv("TSQR_LOOKAHEAD");
+    if (la && std::atoi(la) != 0 && tsqr_set_lookahead(p, 1) != TSQR_OK) {
+      delete p;
+      return TSQR_ERR_CUDA;
+    }
+  }
   *plan = p;
   return TSQR_OK;
 }
@@ -1302,6 +1340,30 @@ tsqr_status tsqr_timing(tsqr_plan_t P, int32_t kclass, double* ms, int64_t* laun
 tsqr_status tsqr_data_plane(tsqr_plan_t P, int32_t* plane) {
   if (!P || !plane) return TSQR_ERR_INVALID_ARG;
   *plane = P->L.ar_on ? TSQR_PLANE_FUSED : (P->comm ? TSQR_PLANE_NCCL : TSQR_PLANE_LOCAL);
+  return TSQR_OK;
+}
+
+tsqr_status tsqr_set_lookahead(tsqr_plan_t P, int32_t enable) {
+  if (!P) return TSQR_ERR_INVALID_ARG;
+  // mCQR2GS only (the adaptive variant's skip mark is a plan-wide status word the concurrent
+  // trailing update would see); the streaming path only
+  const bool on = enable != 0 && P->algo == TSQR_MCQR2GS && !P->cluster && P->k > 2;
+  if (on && !P->side) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+    for (int j = 0; j < P->k; ++j) {
+      cudaEvent_t a, b;
+      CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      P->ev_fork.push_back(a);
+      P->ev_join.push_back(b);
+    }
+  }
+  if (on != P->lookahead && P->exec) {  // the schedule is baked into the captured graph
+    CUDA_TRY(cudaStreamSynchronize(P->gstream));
+    cudaGraphExecDestroy(P->exec);
+    P->exec = nullptr;
+  }
+  P->lookahead = on;
   return TSQR_OK;
 }
 

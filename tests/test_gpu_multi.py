@@ -34,9 +34,10 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, m_local, n, b, kappa, algo, cuts=None, plane="fused", reps=1):
+def _worker(rank, world, port, q, m_local, n, b, kappa, algo, cuts=None, plane="fused", reps=1, la=False):
     import sys
     sys.path.insert(0, ROOT)
+    os.environ["TSQR_LOOKAHEAD"] = "1" if la else "0"
     os.environ["TSQR_FUSED_ALLREDUCE"] = "1" if plane == "fused" else "0"
     os.environ["TSQR_NCCL_ALLREDUCE"] = "1" if plane == "nccl" else "0"
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -145,14 +146,23 @@ def _world():
     return min(_ngpu(), 8)
 
 
-def _run_ranks(algo, n, b, kappa, cuts=None, plane="fused", reps=3):
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("plane", PLANES)
+def test_lookahead_multi_rank(plane):
+    """NEXT-f1 look-ahead across ranks: the panel chain's cross-GPU sums run on the second
+    stream while the trailing update proceeds; results as every other case (oracle, gates,
+    bitwise-replicated R)."""
+    _run_ranks("mcqr2gs", 512, 64, 1e15, plane=plane, la=True)
+
+
+def _run_ranks(algo, n, b, kappa, cuts=None, plane="fused", reps=3, la=False):
     import torch.multiprocessing as mp
     world = _world()
     m_local = 1 << 16
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, m_local, n, b, kappa, algo, cuts, plane, reps))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, m_local, n, b, kappa, algo, cuts, plane, reps, la))
              for r in range(world)]
     for p in procs:
         p.start()

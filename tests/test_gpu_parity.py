@@ -508,3 +508,29 @@ def test_full_size_cfg4_in_bench_configuration(T, orc, b):
     _, R11, info = orc.factor(A1, b, "cqr2")
     assert info["status"] == 0
     assert np.linalg.norm(Rh[:b, :b] - R11) / np.linalg.norm(R11) <= 1e-10
+
+
+@pytest.mark.parametrize("m,n,b,kappa", [(65536 + 37, 512, 64, 1e15), (20000, 1024, 128, 1e8), (8192, 256, 32, 1e12),
+                                         (30000, 1536, 512, 1e6)])
+def test_lookahead_bitwise_equals_serial(T, m, n, b, kappa):
+    """NEXT-f1 look-ahead: panel j's CholeskyQR chain on a second stream under the
+    trailing update -- the same kernels on the same operands, so Q and R are bitwise those of
+    the serial schedule, over graph replays and in eager mode."""
+    import torch
+    A, _, _ = synth.generate_np(m, n, kappa, seed=10, chunk=m if m % 65536 else 65536)
+    A0 = T.to_colmajor(A)
+    outs = []
+    for la, graph in ((False, True), (True, True), (True, False)):
+        p = T.Plan(m, n, b, "mcqr2gs")
+        p.set_lookahead(la)
+        p.set_graph(graph)
+        X = T.colmajor_empty(m, n)
+        for _ in range(3 if graph else 1):
+            X.copy_(A0)
+            R = p.factor(X)
+        assert p.counts()[0] == 4 * (n // b) - 2
+        outs.append((X.cpu().numpy(), R.cpu().numpy()))
+        p.close()
+    torch.cuda.synchronize()
+    for q, r in outs[1:]:
+        assert np.array_equal(q, outs[0][0]) and np.array_equal(r, outs[0][1])
