@@ -238,6 +238,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-graph", action="store_true", help="launch kernels eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--lookahead", action="store_true",
+                    help="NEXT-f1: panel CholeskyQR chain on a second stream under the trailing update")
+    ap.add_argument("--algo", default=None, help="override the config's algorithm (e.g. mcqr2gs_adaptive)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -266,6 +269,8 @@ def main():
         comm = tsqr.NcclComm(rank, world, local)
 
     m_local, n, b, kappa, algo, desc = cfg
+    if args.algo:
+        algo, desc = args.algo, desc + f" [algo {args.algo}]"
     strong = args.config in STRONG
     if strong:  # fixed global problem split over the ranks
         m_global = m_local
@@ -286,6 +291,8 @@ def main():
     plan = tsqr.Plan(m_local, n, b, algo, comm=comm, stream=stream, device=dev)
     if args.no_graph:
         plan.set_graph(False)
+    if args.lookahead:
+        plan.set_lookahead(True)
 
     def barrier():
         if world > 1:
@@ -417,6 +424,7 @@ def main():
             "gpu_launches": launches * args.steps,
             "allreduces_per_step": allreduces,
             "exec_path": plan.exec_path(),
+            "lookahead": bool(args.lookahead),
             "clocks": clk,
             "rows_per_s": m_global * args.steps / (total_ms / 1e3),
             "per_gpu_tflops": value / world,

@@ -281,6 +281,12 @@ struct Launcher {
   ncclWindow_t ar_win = nullptr;
   int ar_nranks = 1, ar_rank = 0;
   int64_t ar_cap = 0;  // doubles per rank slot of the window (b * n: the largest summed block)
+  // Blocks above this many doubles take k_reduce + ncclAllReduce even on the fused plane: the
+  // fused kernel's element-wise peer stores suit the <= 224 KiB blocks of the weak-scaling
+  // configurations, NCCL's bandwidth algorithms the 100+ MB blocks of the wide panels (NEXT-f3).
+  // A function of the block shape only -> the same choice on every rank.
+  int64_t ar_fuse_max = int64_t(1) << 20;
+  bool fuse(int64_t count) const { return ar_on && count <= ar_fuse_max; }
 
   // OUT (p x q, ldo) = L^T R summed over all m rows (split-row partials + fixed-order reduce);
   // with `global` and the fused path on: summed over every rank as well (one kernel)
@@ -308,7 +314,7 @@ struct Launcher {
     }
     CUDA_TRY(cudaGetLastError());
     launches += 1;
-    if (global && ar_on) {
+    if (global && fuse((int64_t)p * q)) {
       if (gram) tend(t0, TSQR_KCLASS_GRAM, (double)m * p * p, 8.0 * m * p);
       else tend(t0, TSQR_KCLASS_PROJ, 2.0 * m * p * q, 8.0 * m * (p + q));
       const size_t t1 = tbegin();
@@ -715,7 +721,7 @@ tsqr_status panel_done(tsqr_plan_s* P, int j) {
 // W <- allreduce(X^T X), X = m x w slab (standalone split-row Gram)
 tsqr_status gram(tsqr_plan_s* P, const double* X, int64_t ldx, int w) {
   TRY(P->L.atb(X, ldx, X, ldx, P->m, w, w, true, P->part, P->W, w, true));
-  if (P->L.ar_on) { P->allreduces++; return TSQR_OK; }
+  if (P->L.fuse((int64_t)w * w)) { P->allreduces++; return TSQR_OK; }
   return allreduce(P, P->W, (size_t)w * w);
 }
 
@@ -740,7 +746,7 @@ tsqr_status cqr(tsqr_plan_s* P, double* X, int64_t ldx, int w, double* Uout, int
 // OUT (p x q, ld p) <- allreduce(L^T Rm)
 tsqr_status proj(tsqr_plan_s* P, const double* Lm, int64_t ldl, int p, const double* Rm, int64_t ldr, int q, double* out) {
   TRY(P->L.atb(Lm, ldl, Rm, ldr, P->m, p, q, false, P->part, out, p, true));
-  if (P->L.ar_on) { P->allreduces++; return TSQR_OK; }
+  if (P->L.fuse((int64_t)p * q)) { P->allreduces++; return TSQR_OK; }
   return allreduce(P, out, (size_t)p * q);
 }
 
@@ -909,6 +915,7 @@ tsqr_status setup_fused_allreduce(tsqr_plan_s* p) {
   p->L.ar_nranks = p->nranks;
   p->L.ar_rank = p->rank;
   p->L.ar_cap = (int64_t)count;
+  if (const char* fm = std::getenv("TSQR_FUSE_MAX")) p->L.ar_fuse_max = std::atoll(fm);  // A/B knob (same on all ranks)
   return TSQR_OK;
 }
 
