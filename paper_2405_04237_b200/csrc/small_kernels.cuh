@@ -338,72 +338,6 @@ __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_diag(const double* __restri
   blk_store(Z + (int64_t)J * CHB * ldz + J * CHB, ldz, Di, tid);
 }
 
-// The diagonal step of the wide-panel Cholesky is its serial chain (nb of them per factorisation),
-// so it is latency-tuned: 64 threads, thread c holds column c of W_JJ in registers, the pivot row
-// is broadcast through shared memory (named barrier over the 2 warps), one rsqrt per pivot
-// (u_kk = d rsqrt(d)); then Z_JJ = U_JJ^{-1} column by column (thread c, back substitution from
-// a shared copy of U_JJ, reusing the registers).  ~10x fewer cycles than the 512-thread block
-// primitives (the FP64 latency chain, `tools/microbench/chol_variants.cu`).
-__device__ __forceinline__ void bar64() { asm volatile("bar.sync 1, 64;\n" ::: "memory"); }
-
-__global__ void __launch_bounds__(64, 1) k_chol_diag64(const double* __restrict__ work, int b, int J,
-                                                       double* __restrict__ U, int ldu, double* __restrict__ Z,
-                                                       int ldz, int* status, int pass, int panel, int stage) {
-  __shared__ double row[CHB];
-  __shared__ double Us[CHB * CHLD];
-  __shared__ int s_bad;
-  if (failed(status)) return;
-  const int c = threadIdx.x;
-  const double* Wb = work + (int64_t)J * CHB + (int64_t)J * CHB * b;
-  double x[CHB];
-#pragma unroll
-  for (int i = 0; i < CHB; ++i) x[i] = (i <= c) ? Wb[i + (int64_t)c * b] : 0.0;
-  int bad = -1;
-  double dbad = 0.0;
-#pragma unroll
-  for (int k = 0; k < CHB; ++k) {
-    if (c == k) row[k] = x[k];
-    bar64();
-    const double d = row[k];
-    if (bad < 0 && (!(d > 0.0) || !isfinite(d))) { bad = k; dbad = d; }
-    const double r = rsqrt(d), ukk = d * r;
-    const double ukj = (c == k) ? ukk : x[k] * r;
-    if (c >= k) x[k] = ukj;
-    if (c > k) row[c] = ukj;
-    bar64();
-#pragma unroll
-    for (int i = k + 1; i < CHB; ++i)
-      if (c >= i) x[i] = fma(-row[i], ukj, x[i]);
-    bar64();
-  }
-  if (c == 0) s_bad = bad;
-  if (bad >= 0 && c == 0) {
-    status[1] = pass; status[2] = panel; status[3] = stage; status[4] = J * CHB + bad;
-    *reinterpret_cast<double*>(status + 6) = dbad;
-    __threadfence();
-    status[0] = 5;
-  }
-#pragma unroll
-  for (int i = 0; i < CHB; ++i) {
-    const double v = (i <= c) ? x[i] : 0.0;
-    Us[i + c * CHLD] = v;
-    U[(int64_t)J * CHB + i + ((int64_t)J * CHB + c) * ldu] = v;
-  }
-  bar64();
-  if (s_bad >= 0) return;
-  // column c of Z_JJ: z_i = (delta_ic - sum_{t=i+1..c} U_it z_t) / U_ii, i = c .. 0
-#pragma unroll
-  for (int i = CHB - 1; i >= 0; --i) {
-    double sacc = 0.0;
-#pragma unroll
-    for (int t = i + 1; t < CHB; ++t)
-      if (t <= c) sacc = fma(Us[i + t * CHLD], x[t], sacc);
-    x[i] = (i <= c) ? (((i == c) ? 1.0 : 0.0) - sacc) / Us[i + i * CHLD] : 0.0;
-  }
-#pragma unroll
-  for (int i = 0; i < CHB; ++i) Z[(int64_t)J * CHB + i + ((int64_t)J * CHB + c) * ldz] = x[i];
-}
-
 __global__ void __launch_bounds__(CHOL_NT, 1) k_chol_row(const double* __restrict__ work, int b, int J,
                                                          double* __restrict__ U, int ldu, const double* __restrict__ Z,
                                                          int ldz, const int* status) {

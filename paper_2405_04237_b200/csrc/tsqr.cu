@@ -446,7 +446,7 @@ struct Launcher {
       k_chol_prep<<<grid_1d((int64_t)b * b), 256, 0, st>>>(W, ldw, b, work, U, ldu, Z, ldz, status_rw);
       launches += 1;
       for (int J = 0; J < nb; ++J) {
-        k_chol_diag64<<<1, 64, 0, st>>>(work, b, J, U, ldu, Z, ldz, status_rw, pass, panel, stage);
+        k_chol_diag<<<1, CHOL_NT, CHOL_BLK_SMEM, st>>>(work, b, J, U, ldu, Z, ldz, status_rw, pass, panel, stage);
         const int r = nb - J - 1;
         if (r > 0) {
           k_chol_row<<<r, CHOL_NT, CHOL_BLK_SMEM, st>>>(work, b, J, U, ldu, Z, ldz, status_rw);
