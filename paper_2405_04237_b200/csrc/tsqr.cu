@@ -1276,7 +1276,7 @@ tsqr_status tsqr_factor_host(tsqr_plan_t P, double* A_host, int64_t lda_host, do
   // the panel-wise methods finalise Q one panel at a time: copy Q_j back on a second stream as
   // soon as it is final, overlapping the remaining panels (H2D has to complete first: the first
   // projection reads every column)
-  const bool by_panel = P->m > 0 && P->k > 1 &&
+  const bool by_panel = P->m > 0 && P->k > 1 && !P->cluster &&  // one launch: nothing to overlap
                         (P->algo == TSQR_MCQR2GS || P->algo == TSQR_MCQR2GS_ADAPTIVE || P->algo == TSQR_CQR2GS);
   if (!P->d2h) {
     CUDA_TRY(cudaStreamCreateWithFlags(&P->d2h, cudaStreamNonBlocking));
