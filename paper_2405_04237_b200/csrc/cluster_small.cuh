@@ -371,7 +371,17 @@ struct ClusterRun {
 
   // Gram of X[:, c0:c0+B], cluster sum -> W (s.red); optional sCQR shift; Cholesky -> U in
   // s.red; X_c <- X_c U^{-1}.  keep: copy U to `keep` (ld B) as well.
+  // B = 16 (cfg1) inlines the CholeskyQR at every call site (measured 0.125 vs 0.149 ms/step
+  // outlined); wider B are outlined: fully inlined, the unrolled trsm / Cholesky bodies of every
+  // call site made the library take ~14 minutes to compile.
   __device__ bool cqr(int c0, int pass, int panel, int stage, double* keep = nullptr, bool shift = false) {
+    if constexpr (B == 16) return cqr_body(c0, pass, panel, stage, keep, shift);
+    else return cqr_outlined(c0, pass, panel, stage, keep, shift);
+  }
+  __device__ __noinline__ bool cqr_outlined(int c0, int pass, int panel, int stage, double* keep, bool shift) {
+    return cqr_body(c0, pass, panel, stage, keep, shift);
+  }
+  __device__ __forceinline__ bool cqr_body(int c0, int pass, int panel, int stage, double* keep, bool shift) {
     cl_atb_local<B>(s, a.ldx, a.mr, c0, B, c0, B);
     CLP(1);
     cl_reduce(cl, s.part, s.red, B * B);
